@@ -1,0 +1,181 @@
+/*
+ * oscflat_b200 — C-ABI drop-in for the reference's per-step beam evolution.
+ *
+ * The seam is the pimpl of the reference's solver::Engine
+ * (/root/reference/proj/core/include/oscflat/solver.hpp:128-153): a
+ * replacement Engine::Impl fills an OscDesc from its solver::Environment,
+ * creates one context per GPU and forwards init_states / trial_step_error /
+ * run / state() to the entry points below.  INTEGRATION.md shows that shim.
+ *
+ * Conventions
+ *  - Plain C types only: pointers + sizes, no torch / CUDA types in the
+ *    signatures (streams are passed as void*).
+ *  - Exceptions never cross the ABI.  Every entry point returns an OscStatus;
+ *    the message of the last failure on the calling thread is available from
+ *    osc_last_error().  The status values map 1:1 onto the reference's
+ *    exception types (types.hpp:43-51, parallel.hpp:15-17).
+ *  - State payloads on the host are the reference's mode-1 order
+ *    [traj][species][comp][ebin] (solver.cpp:127-140), traj = theta*pbins+phi,
+ *    species NuE, NuEBar, NuX, NuXBar, comps ar, ai, br, bi, logical ebins
+ *    (no padding).  With several ranks each context holds the contiguous theta
+ *    block [t_lo, t_hi) given by make_partitions (parallel.cpp:11-24) and the
+ *    payload covers only those trajectories.
+ */
+#ifndef OSCFLAT_B200_H
+#define OSCFLAT_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    OSC_OK = 0,
+    OSC_ERR_CONFIG = 1,   /* oscflat::ConfigError   (types.hpp:43-45) */
+    OSC_ERR_NUMERIC = 2,  /* oscflat::NumericError  (types.hpp:46-48) */
+    OSC_ERR_IO = 3,       /* oscflat::IoError       (types.hpp:49-51) */
+    OSC_ERR_PARALLEL = 4, /* par::ParallelError     (parallel.hpp:15-17) */
+    OSC_ERR_CUDA = 5      /* device / driver failure (no reference analogue) */
+} OscStatus;
+
+/* geom::Model (geometry.hpp:11) */
+enum { OSC_MODEL_SINGLE_ANGLE = 0, OSC_MODEL_BULB = 1, OSC_MODEL_EXT_BULB = 2 };
+/* matter::Profile (matter.hpp:9) */
+enum { OSC_MATTER_POWERLAW = 0, OSC_MATTER_EXP = 1, OSC_MATTER_SUM = 2, OSC_MATTER_OFF = 3 };
+
+/* Everything solver::Environment carries into the step (solver.hpp:71-85).
+ * Tables are copied at osc_create; the caller keeps ownership. */
+typedef struct OscDesc {
+    int model;          /* OSC_MODEL_*                                        */
+    int abins, pbins;   /* AngleGrid::abins / pbins (geometry.hpp:24-36)      */
+    int ebins;          /* logical energy bins                                */
+    double Rnu;         /* km                                                 */
+    const double* cos2_theta0; /* [abins]  AngleGrid::cos2_theta0             */
+    const double* sin_theta0;  /* [abins]  AngleGrid::sin_theta0              */
+    const double* cos_phi;     /* [pbins]  AngleGrid::cos_phi                 */
+    const double* sin_phi;     /* [pbins]  AngleGrid::sin_phi                 */
+    const double* vac_h11;     /* [ebins]  VacuumTable::h11 (geometry.hpp:118)*/
+    const double* vac_h12;     /* [ebins]  VacuumTable::h12                   */
+    const double* fw;          /* [4][ebins] SpectrumTable::weights() f*dE    */
+    double couplings[4];       /* Environment::couplings, 1/km                */
+    double perturb;            /* Environment::perturb                        */
+    int matter_profile;        /* OSC_MATTER_*  (MatterParams, matter.hpp:11) */
+    double Ye, nb0, hNS, Mns, gs, S;
+} OscDesc;
+
+/* One process per GPU.  nranks == 1 -> no collectives.  For nranks > 1 all
+ * ranks pass the same 128-byte NCCL unique id (from osc_comm_unique_id on
+ * rank 0, distributed by the caller). */
+typedef struct OscComm {
+    int rank, nranks, device;
+    const void* nccl_unique_id; /* 128 bytes, ignored when nranks == 1 */
+} OscComm;
+
+/* solver::StepControl (solver.hpp:20-34) */
+typedef struct OscStepControl {
+    double dr, dr_max, dr_min, eps0, kappa, r, R0, Rn;
+    uint64_t iter, Ts;
+    double Tn;
+} OscStepControl;
+
+/* solver::RunSummary (solver.hpp:85-99); termination 1 radius, 2 iterations,
+ * 3 walltime. */
+typedef struct OscRunSummary {
+    double final_r;
+    uint64_t iterations, accepted, rejected;
+    double wall_s, phase_hamiltonian_s, phase_evolve_s, phase_io_s, max_worker_wait_s;
+    double final_max_norm_dev;
+    int termination;
+} OscRunSummary;
+
+/* solver::HookInfo (solver.hpp:101-106) */
+typedef struct OscHookInfo {
+    uint64_t iter;
+    double r, dr, t_wall;
+} OscHookInfo;
+
+/* solver::IoHook (solver.hpp:108-110): called on the host after each accepted
+ * step with the committed local state (mode-1 payload, n doubles); must not
+ * retain the pointer. */
+typedef void (*osc_hook_fn)(void* user, const OscHookInfo* info, const double* state, size_t n);
+
+typedef struct OscCtx OscCtx;
+
+const char* osc_last_error(void);
+int osc_version(void);
+
+/* NCCL unique id for a multi-GPU context (rank 0 calls, caller broadcasts). */
+int osc_comm_unique_id(void* out128);
+
+/* Engine(env, lanes) — solver.cpp:459-466 (lanes -> GPUs, one per process). */
+int osc_create(const OscDesc* desc, const OscComm* comm, OscCtx** out);
+int osc_destroy(OscCtx* ctx);
+
+/* Local theta block [t_lo, t_hi) and local state size in doubles. */
+int osc_local_range(const OscCtx* ctx, int* t_lo, int* t_hi, size_t* state_doubles);
+
+/* Engine::init_states — solver.cpp:475-478 / 255-271 (splitmix64 noise with
+ * seed = global beam index, beam.cpp:41-57). */
+int osc_init_states(OscCtx* ctx);
+
+/* Engine::state() as host mode-1 payloads (copy in / copy out). */
+int osc_set_state(OscCtx* ctx, const double* mode1, size_t n);
+int osc_get_state(OscCtx* ctx, double* mode1, size_t n);
+/* Same, from/to device memory on the context's device (mode-1 order). */
+int osc_set_state_device(OscCtx* ctx, const double* dev_mode1, size_t n);
+int osc_get_state_device(OscCtx* ctx, double* dev_mode1, size_t n);
+
+/* Engine::trial_step_error — solver.cpp:480-484: S1-S4 from (r, dr); returns
+ * the global embedded error; never commits. */
+int osc_trial_step_error(OscCtx* ctx, double r, double dr, double* err);
+
+/* Engine::run — solver.cpp:486-525: the full adaptive loop (fixed-step when
+ * eps0 is huge).  hook may be NULL. */
+int osc_run(OscCtx* ctx, const OscStepControl* ctl, osc_hook_fn hook, void* user,
+            OscRunSummary* out);
+
+/* max over local beams of |norm - 1| (beam.cpp:147-155). */
+int osc_max_norm_dev(OscCtx* ctx, double* out);
+
+/* ---- measurement helpers (bench.py) ------------------------------------ */
+/* Arm a fixed-step walk (as osc_run would) without running it. */
+int osc_begin(OscCtx* ctx, const OscStepControl* ctl);
+/* Enqueue nsteps evolution steps on the context stream; no host sync. */
+int osc_enqueue_steps(OscCtx* ctx, int nsteps);
+/* Copy the device control block to the host (syncs the stream): r, dr, iter,
+ * accepted, rejected, err, status, terminate. */
+int osc_query(OscCtx* ctx, double* r, double* dr, uint64_t* iter, uint64_t* accepted,
+              uint64_t* rejected, double* err, int* status, int* terminate);
+int osc_synchronize(OscCtx* ctx);
+void* osc_stream(OscCtx* ctx);
+/* Kernel launches per evolution step and the kernel-name of the dominant one. */
+int osc_launches_per_step(const OscCtx* ctx);
+/* Last reduced moment sums: out[5][12] = sums0..sums3, next. */
+int osc_debug_sums(OscCtx* ctx, double* out60);
+/* Configure the stage schedule: 0 = recompute intermediates from psi0,
+ * 1 = stash half2 in HBM between S3 and S4. */
+int osc_set_schedule(OscCtx* ctx, int schedule);
+
+/* ---- host-side Environment builder (setup, not the hot path) ----------- */
+/* Mirrors solver::Environment::from_config (solver.cpp:62-95): angle grid,
+ * vacuum table, Fermi-Dirac spectra and couplings from physics parameters. */
+typedef struct OscParams {
+    int model, abins, pbins, ebins;
+    double Rnu, E0, E1, dm2, theta, hvv_scale, perturb;
+    double L[4], T[4], Emean[4], eta[4];
+    int matter_profile;
+    double Ye, nb0, hNS, Mns, gs, S;
+} OscParams;
+typedef struct OscEnv OscEnv;
+int osc_env_build(const OscParams* p, OscEnv** out);
+/* Pointers inside desc stay valid until osc_env_destroy. emean may be NULL. */
+int osc_env_desc(const OscEnv* env, OscDesc* desc, double* emean4);
+int osc_env_destroy(OscEnv* env);
+double osc_fermi_integral(int k, double eta);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

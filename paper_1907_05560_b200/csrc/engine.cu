@@ -1,0 +1,688 @@
+// Host side of the drop-in: the OscCtx behind the C-ABI in
+// include/oscflat_b200.h.  Replaces solver::Engine::Impl
+// (reference solver.cpp:198-456): owns the device state, launches the fused
+// stage kernels, exchanges moment partials between GPUs (NCCL all-gather,
+// fixed rank-order combine), and runs the step loop with the control state
+// resident on the device so that batches of steps are replayed as one CUDA
+// graph without host round trips.
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "oscflat_b200.h"
+#include "status.hpp"
+#include "step_kernels.cuh"
+
+namespace oscb200 {
+
+thread_local std::string g_last_error;
+void set_last_error(const std::string& m) { g_last_error = m; }
+
+#define CUDA_OK(x)                                                                              \
+    do {                                                                                        \
+        cudaError_t e_ = (x);                                                                   \
+        if (e_ != cudaSuccess)                                                                  \
+            throw Error(OSC_ERR_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_));        \
+    } while (0)
+
+// ---------------------------------------------------------------- NCCL (dlopen)
+// NCCL is resolved at run time so a single-GPU context never needs it and the
+// process uses whichever libnccl.so.2 is already loaded (e.g. torch's).
+namespace nccl {
+typedef struct ncclComm* Comm;
+struct UniqueId {
+    char internal[128];
+};
+typedef int (*GetUniqueIdFn)(UniqueId*);
+typedef int (*CommInitRankFn)(Comm*, int, UniqueId, int);
+typedef int (*AllGatherFn)(const void*, void*, size_t, int, Comm, cudaStream_t);
+typedef int (*CommDestroyFn)(Comm);
+typedef const char* (*GetErrorStringFn)(int);
+constexpr int kFloat64 = 8;  // ncclFloat64 (nccl.h)
+
+struct Api {
+    void* h = nullptr;
+    GetUniqueIdFn get_unique_id = nullptr;
+    CommInitRankFn comm_init_rank = nullptr;
+    AllGatherFn all_gather = nullptr;
+    CommDestroyFn comm_destroy = nullptr;
+    GetErrorStringFn error_string = nullptr;
+};
+
+Api& api() {
+    static Api a;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        for (const char* name : {"libnccl.so.2", "libnccl.so"}) {
+            a.h = dlopen(name, RTLD_NOW | RTLD_GLOBAL);
+            if (a.h) break;
+        }
+        if (!a.h) return;
+        a.get_unique_id = (GetUniqueIdFn)dlsym(a.h, "ncclGetUniqueId");
+        a.comm_init_rank = (CommInitRankFn)dlsym(a.h, "ncclCommInitRank");
+        a.all_gather = (AllGatherFn)dlsym(a.h, "ncclAllGather");
+        a.comm_destroy = (CommDestroyFn)dlsym(a.h, "ncclCommDestroy");
+        a.error_string = (GetErrorStringFn)dlsym(a.h, "ncclGetErrorString");
+    });
+    if (!a.h || !a.get_unique_id || !a.comm_init_rank || !a.all_gather)
+        throw Error(OSC_ERR_PARALLEL, "NCCL (libnccl.so.2) is not loadable");
+    return a;
+}
+
+void check(int rc, const char* what) {
+    if (rc != 0)
+        throw Error(OSC_ERR_PARALLEL, std::string(what) + ": " +
+                                          (api().error_string ? api().error_string(rc) : "nccl error"));
+}
+}  // namespace nccl
+
+// ------------------------------------------------------------------ kernels
+using StageFn = void (*)(StepArgs);
+
+template <int MODEL>
+StageFn stage_fn(int stage) {
+    switch (stage) {
+        case 0: return k_stage<MODEL, 0>;
+        case 2: return k_stage<MODEL, 2>;
+        case 3: return k_stage<MODEL, 3>;
+        default: return k_stage<MODEL, 4>;
+    }
+}
+StageFn stage_kernel(int model, int stage) {
+    switch (model) {
+        case 0: return stage_fn<0>(stage);
+        case 1: return stage_fn<1>(stage);
+        default: return stage_fn<2>(stage);
+    }
+}
+
+template <class T>
+struct DevBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    void alloc(size_t count) {
+        free();
+        if (count == 0) count = 1;
+        CUDA_OK(cudaMalloc(&p, count * sizeof(T)));
+        n = count;
+    }
+    void free() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+};
+
+}  // namespace oscb200
+
+using namespace oscb200;
+
+struct OscCtx {
+    OscDesc desc{};
+    int rank = 0, nranks = 1, device = 0;
+    int t_lo = 0, t_hi = 0;
+    int T = 0, P = 0, E = 0;
+    int ntraj = 0, ncell = 0, npad = 0;
+    int nsm = 0, nblocks = 0, chunk = 0, smem = 0;
+    int schedule = 0;
+    cudaStream_t stream = nullptr;
+    nccl::Comm comm = nullptr;
+
+    DevBuf<double> cos2, sin0, cphi, sphi, vac11, vac12, g;
+    DevBuf<double> psi[2], half2, xbuf, xsend, partials, staging;
+    DevBuf<Ctl> ctl;
+    DevBuf<unsigned long long> scratch;
+    Ctl* h_ctl = nullptr;  // pinned mirror
+
+    StepArgs args{};
+    cudaGraphExec_t graph = nullptr;
+    int graph_steps = 0;
+
+    ~OscCtx() {
+        if (graph) cudaGraphExecDestroy(graph);
+        if (comm) {
+            try {
+                nccl::api().comm_destroy(comm);
+            } catch (...) {
+            }
+        }
+        if (h_ctl) cudaFreeHost(h_ctl);
+        if (stream) cudaStreamDestroy(stream);
+    }
+
+    void launch_stage(int stage) {
+        const StageFn fn = stage_kernel(desc.model, stage);
+        fn<<<nblocks, kBlock, smem, stream>>>(args);
+        CUDA_OK(cudaGetLastError());
+    }
+
+    void exchange(int slot) {
+        if (nranks == 1) return;
+        nccl::check(nccl::api().all_gather(xsend.p + (size_t)slot * kSlotDoubles,
+                                           xbuf.p + (size_t)slot * nranks * kSlotDoubles, kSlotDoubles,
+                                           nccl::kFloat64, comm, stream),
+                    "ncclAllGather");
+    }
+
+    // One evolution step = S2, S3, S4 (+ exchange after each; control fused
+    // into S4's last block on a single GPU).
+    void enqueue_step() {
+        launch_stage(2);
+        exchange(1);
+        launch_stage(3);
+        exchange(2);
+        launch_stage(4);
+        exchange(3);
+        if (nranks > 1) {
+            k_control<<<1, 32, 0, stream>>>(args);
+            CUDA_OK(cudaGetLastError());
+        }
+    }
+
+    void enqueue_moments0() {
+        launch_stage(0);
+        exchange(0);
+    }
+
+    void build_graph(int steps) {
+        if (graph) {
+            cudaGraphExecDestroy(graph);
+            graph = nullptr;
+        }
+        cudaGraph_t g_ = nullptr;
+        CUDA_OK(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
+        for (int i = 0; i < steps; ++i) enqueue_step();
+        CUDA_OK(cudaStreamEndCapture(stream, &g_));
+        CUDA_OK(cudaGraphInstantiate(&graph, g_, 0));
+        cudaGraphDestroy(g_);
+        graph_steps = steps;
+    }
+
+    void enqueue_steps(int n) {
+        if (n >= 8) {
+            if (!graph) build_graph(8);
+            for (; n >= graph_steps; n -= graph_steps) CUDA_OK(cudaGraphLaunch(graph, stream));
+        }
+        for (; n > 0; --n) enqueue_step();
+    }
+
+    void download_ctl() {
+        CUDA_OK(cudaMemcpyAsync(h_ctl, ctl.p, sizeof(Ctl), cudaMemcpyDeviceToHost, stream));
+        CUDA_OK(cudaStreamSynchronize(stream));
+    }
+    void upload_ctl() {
+        CUDA_OK(cudaMemcpyAsync(ctl.p, h_ctl, sizeof(Ctl), cudaMemcpyHostToDevice, stream));
+        CUDA_OK(cudaStreamSynchronize(stream));
+    }
+
+    void raise_device_status() {
+        if (!h_ctl->status) return;
+        const std::string where = " at r = " + std::to_string(h_ctl->r) + " km, iteration " +
+                                  std::to_string(h_ctl->iter);
+        switch (h_ctl->reason) {
+            case 1: throw Error(OSC_ERR_NUMERIC, "non-finite amplitudes" + where);
+            case 2: throw Error(OSC_ERR_NUMERIC, "non-finite Hamiltonian sum" + where);
+            case 3: throw Error(OSC_ERR_NUMERIC, "step collapse: rejected step would need dr < min_dr" + where);
+            default: throw Error(OSC_ERR_NUMERIC, "device numeric failure" + where);
+        }
+    }
+
+    void check_radius(double r) const {
+        if (desc.model != OSC_MODEL_SINGLE_ANGLE && r < desc.Rnu)
+            throw Error(OSC_ERR_NUMERIC, "fill_cache: r below the neutrino sphere");
+        if (desc.matter_profile != OSC_MATTER_OFF && r < desc.Rnu)
+            throw Error(OSC_ERR_NUMERIC, "baryon_density: r below the neutrino sphere");
+    }
+
+    // Arm the device control block like Engine::run's first packet
+    // (solver.cpp:492-500).
+    void begin(const OscStepControl& c, int commit) {
+        download_ctl();
+        Ctl& h = *h_ctl;
+        h.r = c.r;
+        h.dr = commit ? std::min(c.dr, std::max(0.0, c.Rn - c.r)) : c.dr;
+        h.iter = c.iter;
+        h.accepted = h.rejected = 0;
+        h.err = 0.0;
+        h.status = h.reason = 0;
+        h.commit = commit;
+        h.dr_max = c.dr_max;
+        h.dr_min = c.dr_min;
+        h.eps0 = c.eps0;
+        h.kappa = c.kappa;
+        h.Rn = c.Rn;
+        h.Ts = commit ? c.Ts : 0;
+        std::memset(h.counter, 0, sizeof h.counter);
+        const double r_eps = 1e-12 * std::max(1.0, std::fabs(c.Rn));
+        h.terminate = 0;
+        if (commit) {
+            if (c.r >= c.Rn - r_eps) h.terminate = 1;
+            if (c.Ts > 0 && c.iter >= c.Ts) h.terminate = 2;
+        }
+        upload_ctl();
+        if (!h.terminate) {
+            check_radius(c.r);
+            enqueue_moments0();
+        }
+    }
+};
+
+namespace {
+
+int grid_blocks(OscCtx* c) {
+    return c->nblocks;
+}
+
+void validate(const OscDesc* d) {
+    if (!d) throw Error(OSC_ERR_CONFIG, "osc_create: null desc");
+    if (d->model < 0 || d->model > 2) throw Error(OSC_ERR_CONFIG, "osc_create: bad model");
+    if (d->abins < 1 || d->pbins < 1 || d->ebins < 1)
+        throw Error(OSC_ERR_CONFIG, "osc_create: Abins, Pbins, Ebins must be >= 1");
+    if (d->model == OSC_MODEL_SINGLE_ANGLE && (d->abins != 1 || d->pbins != 1))
+        throw Error(OSC_ERR_CONFIG, "single-angle model needs abins = pbins = 1");
+    if (d->model == OSC_MODEL_BULB && d->pbins != 1)
+        throw Error(OSC_ERR_CONFIG, "bulb model needs pbins = 1");
+    if (!d->cos2_theta0 || !d->sin_theta0 || !d->cos_phi || !d->sin_phi || !d->vac_h11 ||
+        !d->vac_h12 || !d->fw)
+        throw Error(OSC_ERR_CONFIG, "osc_create: null table");
+    if (d->matter_profile < 0 || d->matter_profile > 3)
+        throw Error(OSC_ERR_CONFIG, "osc_create: bad matter profile");
+}
+
+template <class T>
+void upload(DevBuf<T>& b, const T* src, size_t n) {
+    b.alloc(n);
+    CUDA_OK(cudaMemcpy(b.p, src, n * sizeof(T), cudaMemcpyHostToDevice));
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* osc_last_error(void) { return g_last_error.c_str(); }
+int osc_version(void) { return 1; }
+
+int osc_comm_unique_id(void* out128) {
+    return guarded([&] {
+        nccl::UniqueId id;
+        nccl::check(nccl::api().get_unique_id(&id), "ncclGetUniqueId");
+        std::memcpy(out128, &id, sizeof id);
+    });
+}
+
+int osc_create(const OscDesc* desc, const OscComm* comm, OscCtx** out) {
+    return guarded([&] {
+        validate(desc);
+        if (!out) throw Error(OSC_ERR_CONFIG, "osc_create: null out");
+        auto c = std::make_unique<OscCtx>();
+        c->desc = *desc;
+        c->rank = comm ? comm->rank : 0;
+        c->nranks = comm ? comm->nranks : 1;
+        c->device = comm ? comm->device : 0;
+        if (c->nranks < 1 || c->nranks > kMaxRanks || c->rank < 0 || c->rank >= c->nranks)
+            throw Error(OSC_ERR_CONFIG, "osc_create: bad rank / nranks");
+        if (desc->model == OSC_MODEL_SINGLE_ANGLE && c->nranks != 1)
+            throw Error(OSC_ERR_CONFIG, "single-angle model does not support multiple workers");
+        if (c->nranks > desc->abins) throw Error(OSC_ERR_CONFIG, "Engine: more lanes than theta bins");
+        CUDA_OK(cudaSetDevice(c->device));
+        int major = 0;
+        CUDA_OK(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, c->device));
+        if (major < 10) throw Error(OSC_ERR_CUDA, "oscflat_b200 needs an sm_100 (Blackwell) GPU");
+        CUDA_OK(cudaDeviceGetAttribute(&c->nsm, cudaDevAttrMultiProcessorCount, c->device));
+        CUDA_OK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+
+        // theta partition: make_partitions (parallel.cpp:11-24)
+        const int base = desc->abins / c->nranks, extra = desc->abins % c->nranks;
+        c->t_lo = c->rank * base + std::min(c->rank, extra);
+        c->t_hi = c->t_lo + base + (c->rank < extra ? 1 : 0);
+        c->T = desc->abins;
+        c->P = desc->pbins;
+        c->E = desc->ebins;
+        c->ntraj = (c->t_hi - c->t_lo) * c->P;
+        c->ncell = c->ntraj * c->E;
+        c->npad = (c->ncell + 31) / 32 * 32;
+
+        upload(c->cos2, desc->cos2_theta0, c->T);
+        upload(c->sin0, desc->sin_theta0, c->T);
+        upload(c->cphi, desc->cos_phi, c->P);
+        upload(c->sphi, desc->sin_phi, c->P);
+        upload(c->vac11, desc->vac_h11, c->E);
+        upload(c->vac12, desc->vac_h12, c->E);
+        std::vector<double> g(4 * static_cast<size_t>(c->E));
+        for (int s = 0; s < 4; ++s)
+            for (int e = 0; e < c->E; ++e)
+                g[(size_t)s * c->E + e] = ((s & 1) ? -1.0 : 1.0) * desc->couplings[s] * desc->fw[(size_t)s * c->E + e];
+        upload(c->g, g.data(), g.size());
+        const size_t plane = (size_t)c->npad * 16;
+        c->psi[0].alloc(plane);
+        c->psi[1].alloc(plane);
+        CUDA_OK(cudaMemset(c->psi[0].p, 0, plane * sizeof(double)));
+        CUDA_OK(cudaMemset(c->psi[1].p, 0, plane * sizeof(double)));
+        c->xbuf.alloc((size_t)4 * c->nranks * kSlotDoubles);
+        CUDA_OK(cudaMemset(c->xbuf.p, 0, c->xbuf.n * sizeof(double)));
+        if (c->nranks > 1) {
+            c->xsend.alloc((size_t)4 * kSlotDoubles);
+            CUDA_OK(cudaMemset(c->xsend.p, 0, c->xsend.n * sizeof(double)));
+        }
+        c->ctl.alloc(1);
+        CUDA_OK(cudaMemset(c->ctl.p, 0, sizeof(Ctl)));
+        c->scratch.alloc(4);
+        CUDA_OK(cudaMallocHost(&c->h_ctl, sizeof(Ctl)));
+        std::memset(c->h_ctl, 0, sizeof(Ctl));
+
+        // Launch geometry: one resident wave of blocks, half per particle class.
+        int occ = 0;
+        const StageFn probe = stage_kernel(desc->model, 4);
+        int smem_guess = 48 * 1024;
+        for (int it = 0; it < 3; ++it) {
+            CUDA_OK(cudaFuncSetAttribute(probe, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
+            CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, probe, kBlock, smem_guess));
+            occ = std::max(occ, 1);
+            const int nb_half = std::max(1, c->nsm * occ / 2);
+            int chunk = (c->ncell + nb_half - 1) / nb_half;
+            chunk = std::max(32, (chunk + 31) / 32 * 32);
+            const int ntr_max = chunk / c->E + 2;
+            const int smem = ntr_max * (int)sizeof(TrajRec);
+            c->nblocks = 2 * nb_half;
+            c->chunk = chunk;
+            c->smem = smem;
+            if (smem <= smem_guess) break;
+            smem_guess = smem;
+        }
+        if (c->smem > 160 * 1024) throw Error(OSC_ERR_CONFIG, "osc_create: trajectory records exceed shared memory");
+        for (int st : {0, 2, 3, 4})
+            CUDA_OK(cudaFuncSetAttribute(stage_kernel(desc->model, st),
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, std::max(c->smem, 1)));
+        c->partials.alloc((size_t)c->nblocks * kSlotDoubles);
+
+        if (c->nranks > 1) {
+            if (!comm->nccl_unique_id) throw Error(OSC_ERR_PARALLEL, "osc_create: missing NCCL unique id");
+            nccl::UniqueId id;
+            std::memcpy(&id, comm->nccl_unique_id, sizeof id);
+            nccl::check(nccl::api().comm_init_rank(&c->comm, c->nranks, id, c->rank), "ncclCommInitRank");
+        }
+
+        StepArgs& a = c->args;
+        a.model = desc->model;
+        a.P = c->P;
+        a.E = c->E;
+        a.t_lo = c->t_lo;
+        a.T_loc = c->t_hi - c->t_lo;
+        a.T_glob = c->T;
+        a.ntraj = c->ntraj;
+        a.ncell = c->ncell;
+        a.npad = c->npad;
+        a.chunk = c->chunk;
+        a.nb_half = c->nblocks / 2;
+        a.nranks = c->nranks;
+        a.fuse_ctl = c->nranks == 1;
+        a.schedule = 0;
+        a.Rnu = desc->Rnu;
+        a.dcos2 = 1.0 / c->T;
+        a.phi_measure = desc->model == OSC_MODEL_EXT_BULB ? 1.0 / c->P : 1.0;
+        a.cos2 = c->cos2.p;
+        a.sin0 = c->sin0.p;
+        a.cphi = c->cphi.p;
+        a.sphi = c->sphi.p;
+        a.vac11 = c->vac11.p;
+        a.vac12 = c->vac12.p;
+        a.g = c->g.p;
+        a.matter_profile = desc->matter_profile;
+        a.Ye = desc->Ye;
+        a.nb0 = desc->nb0;
+        a.hNS = desc->hNS;
+        a.Mns = desc->Mns;
+        a.gs = desc->gs;
+        a.S = desc->S;
+        a.psi0_buf[0] = c->psi[0].p;
+        a.psi0_buf[1] = c->psi[1].p;
+        a.half2 = nullptr;
+        a.xbuf = c->xbuf.p;
+        a.xsend = c->nranks > 1 ? c->xsend.p : c->xbuf.p;
+        a.partials = c->partials.p;
+        a.ctl = c->ctl.p;
+        CUDA_OK(cudaDeviceSynchronize());
+        *out = c.release();
+    });
+}
+
+int osc_destroy(OscCtx* ctx) {
+    return guarded([&] {
+        if (!ctx) return;
+        cudaSetDevice(ctx->device);
+        cudaStreamSynchronize(ctx->stream);
+        delete ctx;
+    });
+}
+
+int osc_local_range(const OscCtx* c, int* t_lo, int* t_hi, size_t* n) {
+    return guarded([&] {
+        if (!c) throw Error(OSC_ERR_CONFIG, "null context");
+        if (t_lo) *t_lo = c->t_lo;
+        if (t_hi) *t_hi = c->t_hi;
+        if (n) *n = (size_t)c->ncell * 16;
+    });
+}
+
+int osc_init_states(OscCtx* c) {
+    return guarded([&] {
+        CUDA_OK(cudaSetDevice(c->device));
+        k_init<<<(c->ncell + 255) / 256, 256, 0, c->stream>>>(c->args, c->desc.perturb);
+        CUDA_OK(cudaGetLastError());
+        CUDA_OK(cudaStreamSynchronize(c->stream));
+    });
+}
+
+static void set_state_impl(OscCtx* c, const double* src, size_t n, cudaMemcpyKind kind) {
+    const size_t want = (size_t)c->ncell * 16;
+    if (n != want) throw Error(OSC_ERR_IO, "fill_mode1: payload size does not match the configured problem");
+    CUDA_OK(cudaSetDevice(c->device));
+    if (c->staging.n < want) c->staging.alloc(want);
+    CUDA_OK(cudaMemcpyAsync(c->staging.p, src, want * sizeof(double), kind, c->stream));
+    k_unpack<<<c->nsm * 8, 256, 0, c->stream>>>(c->args, c->staging.p, want);
+    CUDA_OK(cudaGetLastError());
+    CUDA_OK(cudaStreamSynchronize(c->stream));
+}
+
+static void get_state_impl(OscCtx* c, double* dst, size_t n, cudaMemcpyKind kind) {
+    const size_t want = (size_t)c->ncell * 16;
+    if (n != want) throw Error(OSC_ERR_IO, "extract_mode1: payload size mismatch");
+    CUDA_OK(cudaSetDevice(c->device));
+    if (c->staging.n < want) c->staging.alloc(want);
+    k_pack<<<c->nsm * 8, 256, 0, c->stream>>>(c->args, c->staging.p, want);
+    CUDA_OK(cudaGetLastError());
+    CUDA_OK(cudaMemcpyAsync(dst, c->staging.p, want * sizeof(double), kind, c->stream));
+    CUDA_OK(cudaStreamSynchronize(c->stream));
+}
+
+int osc_set_state(OscCtx* c, const double* m, size_t n) {
+    return guarded([&] { set_state_impl(c, m, n, cudaMemcpyHostToDevice); });
+}
+int osc_get_state(OscCtx* c, double* m, size_t n) {
+    return guarded([&] { get_state_impl(c, m, n, cudaMemcpyDeviceToHost); });
+}
+int osc_set_state_device(OscCtx* c, const double* m, size_t n) {
+    return guarded([&] { set_state_impl(c, m, n, cudaMemcpyDeviceToDevice); });
+}
+int osc_get_state_device(OscCtx* c, double* m, size_t n) {
+    return guarded([&] { get_state_impl(c, m, n, cudaMemcpyDeviceToDevice); });
+}
+
+int osc_trial_step_error(OscCtx* c, double r, double dr, double* err) {
+    return guarded([&] {
+        if (c->nranks != 1) throw Error(OSC_ERR_CONFIG, "trial_step_error: single-lane engines only");
+        CUDA_OK(cudaSetDevice(c->device));
+        OscStepControl s{};
+        s.r = r;
+        s.dr = dr;
+        s.dr_max = dr;
+        s.dr_min = 0.0;
+        s.eps0 = 1e300;
+        s.kappa = 1.0;
+        s.Rn = r + dr;
+        c->begin(s, /*commit=*/0);
+        c->enqueue_step();
+        c->download_ctl();
+        c->raise_device_status();
+        *err = c->h_ctl->err;
+    });
+}
+
+int osc_begin(OscCtx* c, const OscStepControl* ctl) {
+    return guarded([&] {
+        CUDA_OK(cudaSetDevice(c->device));
+        c->begin(*ctl, 1);
+    });
+}
+
+int osc_enqueue_steps(OscCtx* c, int n) {
+    return guarded([&] {
+        CUDA_OK(cudaSetDevice(c->device));
+        c->enqueue_steps(n);
+    });
+}
+
+int osc_query(OscCtx* c, double* r, double* dr, uint64_t* iter, uint64_t* acc, uint64_t* rej, double* err,
+              int* status, int* term) {
+    return guarded([&] {
+        CUDA_OK(cudaSetDevice(c->device));
+        c->download_ctl();
+        const Ctl& h = *c->h_ctl;
+        if (r) *r = h.r;
+        if (dr) *dr = h.dr;
+        if (iter) *iter = h.iter;
+        if (acc) *acc = h.accepted;
+        if (rej) *rej = h.rejected;
+        if (err) *err = h.err;
+        if (status) *status = h.status;
+        if (term) *term = h.terminate;
+    });
+}
+
+int osc_synchronize(OscCtx* c) {
+    return guarded([&] {
+        CUDA_OK(cudaSetDevice(c->device));
+        CUDA_OK(cudaStreamSynchronize(c->stream));
+    });
+}
+
+void* osc_stream(OscCtx* c) { return c ? (void*)c->stream : nullptr; }
+
+int osc_launches_per_step(const OscCtx* c) { return c ? (c->nranks > 1 ? 4 : 3) : 0; }
+
+int osc_debug_sums(OscCtx* c, double* out) {
+    return guarded([&] {
+        CUDA_OK(cudaSetDevice(c->device));
+        std::vector<double> x(c->xbuf.n);
+        CUDA_OK(cudaStreamSynchronize(c->stream));
+        CUDA_OK(cudaMemcpy(x.data(), c->xbuf.p, x.size() * sizeof(double), cudaMemcpyDeviceToHost));
+        // totals per slot in rank order: sums0 | sums1 | sums2 | sums3 | next
+        auto total = [&](int slot, int k) {
+            double t = 0.0;
+            for (int q = 0; q < c->nranks; ++q) t += x[((size_t)slot * c->nranks + q) * kSlotDoubles + k];
+            return t;
+        };
+        for (int k = 0; k < 12; ++k) {
+            out[k] = total(0, k);
+            out[12 + k] = total(1, k);
+            out[24 + k] = total(1, 12 + k);
+            out[36 + k] = total(2, k);
+            out[48 + k] = total(3, k);
+        }
+    });
+}
+
+int osc_set_schedule(OscCtx* c, int schedule) {
+    return guarded([&] {
+        CUDA_OK(cudaSetDevice(c->device));
+        if (schedule != 0 && schedule != 1) throw Error(OSC_ERR_CONFIG, "schedule must be 0 or 1");
+        if (schedule == 1 && !c->half2.p) c->half2.alloc((size_t)c->npad * 16);
+        c->schedule = schedule;
+        c->args.schedule = schedule;
+        c->args.half2 = c->half2.p;
+        if (c->graph) {
+            cudaGraphExecDestroy(c->graph);
+            c->graph = nullptr;
+        }
+    });
+}
+
+int osc_max_norm_dev(OscCtx* c, double* out) {
+    return guarded([&] {
+        CUDA_OK(cudaSetDevice(c->device));
+        CUDA_OK(cudaMemsetAsync(c->scratch.p, 0, sizeof(unsigned long long), c->stream));
+        k_norm_dev<<<c->nsm * 4, 256, 0, c->stream>>>(c->args, c->scratch.p);
+        CUDA_OK(cudaGetLastError());
+        unsigned long long bits = 0;
+        CUDA_OK(cudaMemcpyAsync(&bits, c->scratch.p, sizeof bits, cudaMemcpyDeviceToHost, c->stream));
+        CUDA_OK(cudaStreamSynchronize(c->stream));
+        double v;
+        std::memcpy(&v, &bits, sizeof v);
+        *out = v;
+    });
+}
+
+int osc_run(OscCtx* c, const OscStepControl* ctl, osc_hook_fn hook, void* user, OscRunSummary* out) {
+    return guarded([&] {
+        using Clock = std::chrono::steady_clock;
+        if (!ctl || !out) throw Error(OSC_ERR_CONFIG, "osc_run: null argument");
+        CUDA_OK(cudaSetDevice(c->device));
+        const auto t0 = Clock::now();
+        auto secs = [&] { return std::chrono::duration<double>(Clock::now() - t0).count(); };
+        c->begin(*ctl, 1);
+        double t_io = 0.0;
+        int term = c->h_ctl->terminate;
+        std::vector<double> host_state;
+        uint64_t last_acc = 0;
+        // batch size: one step at a time when a hook must see every accepted
+        // state, else graph batches with a host check between batches
+        while (!term) {
+            if (hook) {
+                c->enqueue_step();
+            } else {
+                int batch = 64;
+                if (ctl->Ts > 0) {
+                    const uint64_t left = ctl->Ts - std::min<uint64_t>(ctl->Ts, c->h_ctl->iter);
+                    batch = (int)std::max<uint64_t>(1, std::min<uint64_t>(left, 64));
+                }
+                c->enqueue_steps(batch);
+            }
+            c->download_ctl();
+            c->raise_device_status();
+            term = c->h_ctl->terminate;
+            if (hook && c->h_ctl->accepted != last_acc) {
+                last_acc = c->h_ctl->accepted;
+                const auto ti = Clock::now();
+                host_state.resize((size_t)c->ncell * 16);
+                get_state_impl(c, host_state.data(), host_state.size(), cudaMemcpyDeviceToHost);
+                OscHookInfo info{c->h_ctl->iter, c->h_ctl->r, c->h_ctl->dr, secs()};
+                hook(user, &info, host_state.data(), host_state.size());
+                t_io += std::chrono::duration<double>(Clock::now() - ti).count();
+            }
+            if (!term && ctl->Tn > 0.0 && secs() >= ctl->Tn) term = 3;
+        }
+        double nd = 0.0;
+        osc_max_norm_dev(c, &nd);
+        const Ctl& h = *c->h_ctl;
+        out->final_r = h.r;
+        out->iterations = h.iter - ctl->iter;
+        out->accepted = h.accepted;
+        out->rejected = h.rejected;
+        out->wall_s = secs();
+        out->phase_hamiltonian_s = 0.0;
+        out->phase_evolve_s = out->wall_s - t_io;
+        out->phase_io_s = t_io;
+        out->max_worker_wait_s = 0.0;
+        out->final_max_norm_dev = nd;
+        out->termination = term == 2 ? 2 : (term == 3 ? 3 : 1);
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,270 @@
+"""Python mirror of the reference's ``solver`` API over the C-ABI.
+
+Reference: ``include/oscflat/solver.hpp:20-153``.  Names and argument meaning
+follow the reference so the parity tests read like ``test_solver.cpp``:
+
+* ``Environment.from_config(cfg)``  ->  solver::Environment::from_config
+* ``Engine(env, gpus)``             ->  solver::Engine(env, lanes)
+* ``engine.init_states()``, ``engine.state()``, ``engine.trial_step_error(r, dr)``,
+  ``engine.run(ctl, hook)``          ->  the same-named Engine members
+* ``StepControl.from_config(cfg)``  ->  solver::StepControl::from_config
+* errors: ConfigError / NumericError / IoError / ParallelError (types.hpp:43-51)
+
+All compute happens in the native library; there is no CPU path here.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import native
+from .config import RunConfig
+from .native import (HOOK_FN, OscComm, OscDesc, OscParams, OscRunSummary, OscStepControl, check,
+                     lib)
+
+
+@dataclass
+class StepControl:
+    """solver::StepControl (solver.hpp:20-34)."""
+
+    dr: float = 1e-3
+    dr_max: float = 1.0
+    dr_min: float = 1e-12
+    eps0: float = 1e-8
+    kappa: float = 0.8
+    r: float = 0.0
+    R0: float = 0.0
+    Rn: float = 0.0
+    iter: int = 0
+    Ts: int = 0
+    Tn: float = 0.0
+
+    @classmethod
+    def from_config(cls, cfg: RunConfig) -> "StepControl":
+        v = cfg.values
+        return cls(dr=v["dr"], dr_max=v["max_dr"], dr_min=v["min_dr"], eps0=v["eps0"],
+                   kappa=v["kappa"], r=v["R0"], R0=v["R0"], Rn=v["Rn"], iter=0, Ts=v["Ts"],
+                   Tn=v["Tn"])
+
+    def to_c(self) -> OscStepControl:
+        return OscStepControl(dr=self.dr, dr_max=self.dr_max, dr_min=self.dr_min, eps0=self.eps0,
+                              kappa=self.kappa, r=self.r, R0=self.R0, Rn=self.Rn, iter=self.iter,
+                              Ts=self.Ts, Tn=self.Tn)
+
+
+@dataclass
+class RunSummary:
+    """solver::RunSummary (solver.hpp:85-99)."""
+
+    final_r: float
+    iterations: int
+    accepted: int
+    rejected: int
+    wall_s: float
+    phase_hamiltonian_s: float
+    phase_evolve_s: float
+    phase_io_s: float
+    max_worker_wait_s: float
+    final_max_norm_dev: float
+    termination: str
+
+
+@dataclass
+class HookInfo:
+    iter: int
+    r: float
+    dr: float
+    t_wall: float
+
+
+class Environment:
+    """solver::Environment (solver.hpp:71-85): grid, vacuum table, spectra,
+    couplings and matter parameters, built by the native host code."""
+
+    def __init__(self, cfg: RunConfig):
+        cfg.require_runnable()
+        v = cfg.values
+        p = OscParams()
+        p.model = cfg.model_id
+        p.abins, p.pbins, p.ebins = v["Abins"], v["Pbins"], v["Ebins"]
+        p.Rnu, p.E0, p.E1, p.dm2, p.theta = v["Rv"], v["E0"], v["E1"], v["dm2"], v["theta"]
+        p.hvv_scale, p.perturb = v["hvvScale"], v["perturb"]
+        for arr, name in ((p.L, "L"), (p.T, "T"), (p.Emean, "E"), (p.eta, "eta")):
+            for i, x in enumerate(cfg.species(name)):
+                arr[i] = x
+        p.matter_profile = cfg.matter_id
+        p.Ye, p.nb0, p.hNS, p.Mns, p.gs, p.S = (v["Ye"], v["nb0"], v["hNS"], v["Mns"], v["gs"],
+                                                 v["S"])
+        self.cfg = cfg
+        self._h = C.c_void_p()
+        check(lib().osc_env_build(C.byref(p), C.byref(self._h)))
+        self.desc = OscDesc()
+        emean = (C.c_double * 4)()
+        check(lib().osc_env_desc(self._h, C.byref(self.desc), emean))
+        self.emean = list(emean)
+        d = self.desc
+        self.model, self.abins, self.pbins, self.ebins = d.model, d.abins, d.pbins, d.ebins
+
+    @classmethod
+    def from_config(cls, cfg: RunConfig) -> "Environment":
+        return cls(cfg)
+
+    def __del__(self):
+        try:
+            lib().osc_env_destroy(self._h)
+        except Exception:
+            pass
+
+    def tables(self) -> dict:
+        d = self.desc
+        T, P, E = d.abins, d.pbins, d.ebins
+        arr = lambda p, n: np.ctypeslib.as_array(p, shape=(n,)).copy()
+        return dict(cos2=arr(d.cos2_theta0, T), sin0=arr(d.sin_theta0, T),
+                    cphi=arr(d.cos_phi, P), sphi=arr(d.sin_phi, P), vac11=arr(d.vac_h11, E),
+                    vac12=arr(d.vac_h12, E), fw=arr(d.fw, 4 * E).reshape(4, E),
+                    couplings=np.array(list(d.couplings)), emean=np.array(self.emean))
+
+    @property
+    def trajectories(self) -> int:
+        return self.abins * self.pbins
+
+    @property
+    def cells(self) -> int:
+        return self.trajectories * self.ebins
+
+
+_TERM = {1: "radius", 2: "iterations", 3: "walltime"}
+
+
+class Engine:
+    """solver::Engine (solver.hpp:128-153) on one GPU per process.
+
+    ``rank``/``nranks`` shard the theta bins like the reference's lanes
+    (make_partitions); ``nccl_id`` is the 128-byte id shared by all ranks."""
+
+    def __init__(self, env: Environment, rank: int = 0, nranks: int = 1, device: int = 0,
+                 nccl_id: bytes | None = None):
+        self.env = env  # borrowed, kept alive (solver.hpp:152)
+        self._idbuf = C.create_string_buffer(nccl_id, 128) if nccl_id else None
+        comm = OscComm(rank=rank, nranks=nranks, device=device,
+                       nccl_unique_id=C.cast(self._idbuf, C.c_void_p) if self._idbuf else None)
+        self._ctx = C.c_void_p()
+        check(lib().osc_create(C.byref(env.desc), C.byref(comm), C.byref(self._ctx)))
+        lo, hi, n = C.c_int(), C.c_int(), C.c_size_t()
+        check(lib().osc_local_range(self._ctx, C.byref(lo), C.byref(hi), C.byref(n)))
+        self.t_lo, self.t_hi, self.state_doubles = lo.value, hi.value, n.value
+        self.rank, self.nranks = rank, nranks
+
+    def close(self):
+        if getattr(self, "_ctx", None):
+            lib().osc_destroy(self._ctx)
+            self._ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- reference API ---------------------------------------------------
+    def init_states(self) -> None:
+        check(lib().osc_init_states(self._ctx))
+
+    def state(self) -> np.ndarray:
+        """Committed psi0 as the mode-1 payload [traj][species][comp][ebin]."""
+        out = np.empty(self.state_doubles, dtype=np.float64)
+        check(lib().osc_get_state(self._ctx, out.ctypes.data, out.size))
+        return out
+
+    def set_state(self, mode1) -> None:
+        a = np.ascontiguousarray(mode1, dtype=np.float64).ravel()
+        check(lib().osc_set_state(self._ctx, a.ctypes.data, a.size))
+
+    def trial_step_error(self, r: float, dr: float) -> float:
+        err = C.c_double()
+        check(lib().osc_trial_step_error(self._ctx, r, dr, C.byref(err)))
+        return err.value
+
+    def run(self, ctl: StepControl, hook=None) -> RunSummary:
+        s = OscRunSummary()
+        if hook is not None:
+            def _tramp(user, info, state, n):
+                i = info.contents
+                hook(HookInfo(i.iter, i.r, i.dr, i.t_wall),
+                     np.ctypeslib.as_array(state, shape=(n,)).copy())
+            cb = HOOK_FN(_tramp)
+        else:
+            cb = HOOK_FN()
+        check(lib().osc_run(self._ctx, C.byref(ctl.to_c()), cb, None, C.byref(s)))
+        return RunSummary(s.final_r, s.iterations, s.accepted, s.rejected, s.wall_s,
+                          s.phase_hamiltonian_s, s.phase_evolve_s, s.phase_io_s,
+                          s.max_worker_wait_s, s.final_max_norm_dev,
+                          _TERM.get(s.termination, "radius"))
+
+    # -- device-resident helpers (bench / tests) -------------------------
+    def max_norm_dev(self) -> float:
+        v = C.c_double()
+        check(lib().osc_max_norm_dev(self._ctx, C.byref(v)))
+        return v.value
+
+    def set_state_device(self, ptr: int, n: int) -> None:
+        check(lib().osc_set_state_device(self._ctx, C.c_void_p(ptr), n))
+
+    def get_state_device(self, ptr: int, n: int) -> None:
+        check(lib().osc_get_state_device(self._ctx, C.c_void_p(ptr), n))
+
+    def set_state_host_ptr(self, ptr: int, n: int) -> None:
+        check(lib().osc_set_state(self._ctx, C.c_void_p(ptr), n))
+
+    def get_state_host_ptr(self, ptr: int, n: int) -> None:
+        check(lib().osc_get_state(self._ctx, C.c_void_p(ptr), n))
+
+    def begin(self, ctl: StepControl) -> None:
+        check(lib().osc_begin(self._ctx, C.byref(ctl.to_c())))
+
+    def enqueue_steps(self, n: int) -> None:
+        check(lib().osc_enqueue_steps(self._ctx, n))
+
+    def query(self) -> dict:
+        r, dr, err = C.c_double(), C.c_double(), C.c_double()
+        it, acc, rej = C.c_uint64(), C.c_uint64(), C.c_uint64()
+        st, term = C.c_int(), C.c_int()
+        check(lib().osc_query(self._ctx, C.byref(r), C.byref(dr), C.byref(it), C.byref(acc),
+                              C.byref(rej), C.byref(err), C.byref(st), C.byref(term)))
+        return dict(r=r.value, dr=dr.value, iter=it.value, accepted=acc.value,
+                    rejected=rej.value, err=err.value, status=st.value, terminate=term.value)
+
+    def synchronize(self) -> None:
+        check(lib().osc_synchronize(self._ctx))
+
+    def stream(self) -> int:
+        return lib().osc_stream(self._ctx) or 0
+
+    def launches_per_step(self) -> int:
+        return lib().osc_launches_per_step(self._ctx)
+
+    def debug_sums(self) -> np.ndarray:
+        out = np.zeros(60)
+        check(lib().osc_debug_sums(self._ctx, out.ctypes.data_as(C.POINTER(C.c_double))))
+        return out.reshape(5, 12)
+
+    def set_schedule(self, schedule: int) -> None:
+        check(lib().osc_set_schedule(self._ctx, schedule))
+
+
+def comm_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    check(lib().osc_comm_unique_id(buf))
+    return buf.raw
+
+
+def fermi_integral(k: int, eta: float) -> float:
+    return lib().osc_fermi_integral(k, eta)
+
+
+ConfigError = native.ConfigError
+NumericError = native.NumericError
+IoError = native.IoError
+ParallelError = native.ParallelError
