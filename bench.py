@@ -1,0 +1,336 @@
+#!/usr/bin/env python
+"""Benchmark: fp64 beam-steps/s of the fused evolution step on B200.
+
+One "step" = one full S1-S4 evolution step (reference solver.cpp:343-412)
+of every beam of the workload; one beam-step = one (angle, energy) cell with
+all four species (BASELINE.md "Unit").  Default workload: BASELINE.json
+configs[2] (bulb, 4096 angle x 256 energy bins, 2 flavours, fp64, fixed step
+dr = 0.24 km from r = 10 km), the largest single-GPU configuration the
+reference implements.
+
+Arms
+  (default)          our CUDA path; `value` = device-resident throughput
+                     (CUDA events on the engine stream, max over ranks);
+                     `e2e` = the reference-facing call sequence with HOST
+                     buffers: set_state(host psi0) + run(K steps) +
+                     state() -> host, timed on the device stream.
+  --impl reference   the reference's own CPU implementation (oracle/_ref:
+                     the unmodified reference core compiled from its sources)
+                     on this box's host cores, same workload / metric.
+
+Launch: python bench.py --gpus N --steps K --warmup W   (torchrun for N > 1)
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "fp64 beam-steps/sec"
+UNIT = "beam-steps/s"
+
+
+def _args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=400)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="configs2")
+    ap.add_argument("--schedule", type=int, default=-1)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-steps", type=int, default=0)
+    return ap.parse_args()
+
+
+def _dist():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        fd, self.path = tempfile.mkstemp(prefix="clocks_", suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.12)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        rows = []
+        for line in open(self.path):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                rows.append(parts)
+            except ValueError:
+                pass
+        os.unlink(self.path)
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for r in rows for n, v in zip(names, r[5:9]) if v.lower() == "active"})
+        busy = [s for s in sm if s > 0.5 * (max(sm) if sm else 1)]
+        return {"sm_mhz": statistics.median(busy) if busy else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(rows)}
+
+
+# --------------------------------------------------------------- reference
+def _ref_lib():
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import pyoracle  # checker / CPU baseline only
+
+    return pyoracle
+
+
+def cpu_reference(cfg, steps: int, warmup: int):
+    """Time the reference CPU engine (oracle/_ref) on all host cores."""
+    po = _ref_lib()
+    ref = po.Ref()
+    text = cfg.render()
+    T = cfg.values["Abins"]
+    lanes = max(1, min(os.cpu_count() or 1, T))
+    cells = T * cfg.values["Pbins"] * cfg.values["Ebins"]
+    if warmup > 0:
+        ref.run(text, lanes=lanes, ts=warmup)
+    t0 = time.perf_counter()
+    _, summ = ref.run(text, lanes=lanes, ts=steps)
+    wall = time.perf_counter() - t0
+    run_wall = summ["wall_s"]
+    return dict(value=cells * steps / run_wall, cores=lanes, wall=wall, steps=steps,
+                variant=ref.variant, iterations=summ["iterations"])
+
+
+def run_reference_arm(a, cfg):
+    rank, world, _ = _dist()
+    if rank != 0:
+        return
+    try:
+        r = cpu_reference(cfg, a.steps, a.warmup)
+    except Exception as e:  # noqa: BLE001
+        print(json.dumps({"impl": "reference", "unavailable": f"{type(e).__name__}: {e}"}))
+        return
+    cells = cfg.values["Abins"] * cfg.values["Pbins"] * cfg.values["Ebins"]
+    line = {
+        "impl": "reference", "metric": METRIC, "value": r["value"], "unit": UNIT,
+        "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
+        "ms_per_step": 1e3 * cells / r["value"], "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": a.config, "cells": cells, "parallelism": f"{r['cores']} host threads"},
+        "cpu_baseline": {"value": r["value"], "unit": UNIT, "cores": r["cores"],
+                         "kind": "reference",
+                         "sample": f"{a.config}: solver::Engine::run of {a.steps} fixed steps "
+                                   f"from R0 (after {a.warmup} warm-up steps), "
+                                   f"{r['cores']} lanes, build x86-64-{r['variant']}"},
+        "e2e": {"value": r["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------- our arm
+def main():
+    a = _args()
+    from paper_1907_05560_b200 import baseline_config
+
+    cfg = baseline_config(a.config)
+    if a.impl == "reference":
+        run_reference_arm(a, cfg)
+        return
+
+    import torch
+
+    from paper_1907_05560_b200 import Engine, Environment, StepControl, comm_unique_id
+    from paper_1907_05560_b200.engine import fp64_peak
+
+    rank, world, local = _dist()
+    assert world == a.gpus or "RANK" not in os.environ, "--gpus must match WORLD_SIZE"
+    torch.cuda.set_device(local)
+    dist = None
+    nccl_id = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        obj = [comm_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nccl_id = obj[0]
+
+    env = Environment.from_config(cfg)
+    eng = Engine(env, rank=rank, nranks=world, device=local, nccl_id=nccl_id)
+    if a.schedule >= 0:
+        eng.set_schedule(a.schedule)
+    eng.init_states()
+    stream = torch.cuda.ExternalStream(eng.stream())
+    cells_total = env.cells
+    ctl = StepControl.from_config(cfg)
+    ctl.Ts = 0  # the timed walk is bounded by K, not by the config's Ts
+    ctl.Rn = 1e9  # keep walking at max_dr for K steps
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x: float) -> float:
+        if dist is None:
+            return x
+        t = torch.tensor([x], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    sampler = ClockSampler(local)
+    sampler.start()
+    # ---- warm-up (W steps), then exactly K timed steps
+    eng.begin(ctl)
+    eng.enqueue_steps(a.warmup)
+    eng.synchronize()
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    eng.enqueue_steps(a.steps)
+    e1.record(stream)
+    e1.synchronize()
+    barrier()
+    ms = max_over_ranks(e0.elapsed_time(e1))
+    q = eng.query()
+    clocks = sampler.stop()
+    if q["status"] != 0:
+        raise SystemExit(f"device reported status {q['status']}")
+    value = cells_total * a.steps / (ms * 1e-3)
+
+    # ---- per-stage kernel durations (same stream, CUDA events)
+    stage_ms = eng.profile_stages(20) if world == 1 else [None, None, None]
+
+    # ---- e2e through the reference-facing API with host buffers
+    import numpy as np
+
+    n = eng.state_doubles
+    host_in = torch.empty(n, dtype=torch.float64).pin_memory()
+    host_out = torch.empty(n, dtype=torch.float64).pin_memory()
+    eng.get_state_host_ptr(host_in.data_ptr(), n)
+    e2e_steps = a.steps
+    ctl_e2e = StepControl.from_config(cfg)
+    ctl_e2e.Ts = e2e_steps
+    ctl_e2e.Rn = 1e9
+    barrier()
+    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0 = time.perf_counter()
+    f0.record(stream)
+    eng.set_state_host_ptr(host_in.data_ptr(), n)
+    summ = eng.run(ctl_e2e)
+    eng.get_state_host_ptr(host_out.data_ptr(), n)
+    f1.record(stream)
+    f1.synchronize()
+    wall_e2e = time.perf_counter() - t0
+    barrier()
+    ms_e2e = max_over_ranks(max(f0.elapsed_time(f1), wall_e2e * 1e3))
+    e2e_value = cells_total * summ.iterations / (ms_e2e * 1e-3)
+    bytes_state = n * 8
+
+    # ---- roofline (FP64 pipe) for the dominant kernel
+    peak_dfma = fp64_peak(local)  # thread-DFMA/s; 2 flop each
+    W = _work_per_cell()
+    roof = None
+    if stage_ms[0] is not None:
+        names = ["S2", "S3", "S4"]
+        k = max(range(3), key=lambda i: stage_ms[i])
+        w_k = W["per_stage"][names[k]]
+        achieved = w_k * cells_total / (stage_ms[k] * 1e-3) * 2 / 1e12  # TFLOP/s (DFMA-equiv)
+        peak = peak_dfma * 2 / 1e12
+        roof = {"bound": "fp64", "kernel": f"k_stage<{names[k]}>", "achieved": achieved,
+                "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+                "traffic": W.get("traffic", {}).get(names[k]),
+                "work_unit": "FP64 instructions per beam-step (DFMA-equivalent, 2 flop)",
+                "W_per_cell": w_k, "W_source": W["source"],
+                "peak_source": "measured live: DFMA-chain microkernel (osc_fp64_peak)",
+                "stage_ms": dict(zip(names, stage_ms)),
+                "hbm_gbs_S4": (256 * cells_total) / (stage_ms[2] * 1e-3) / 1e9}
+
+    cpu = None
+    if rank == 0 and world == 1 and not a.no_cpu_baseline:
+        try:
+            steps_cpu = a.cpu_steps or max(4, int(40 * 1048576 / cells_total))
+            r = cpu_reference(cfg, steps_cpu, 1)
+            cpu = {"value": r["value"], "unit": UNIT, "cores": r["cores"], "kind": "reference",
+                   "sample": f"{a.config}: reference solver::Engine::run, {steps_cpu} fixed steps "
+                             f"from R0, {r['cores']} lanes, oracle/_ref x86-64-{r['variant']} build"}
+        except Exception as e:  # noqa: BLE001
+            cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
+                   "sample": f"unavailable: {type(e).__name__}: {e}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
+            "warmup": a.warmup, "ms_per_step": ms / a.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": a.config, "cells": cells_total,
+                       "angle_bins": env.abins, "energy_bins": env.ebins, "model": "bulb",
+                       "steps_from_r_km": ctl.r, "dr_km": ctl.dr,
+                       "parallelism": f"theta-sharded x{world}",
+                       "l2": f"inputs larger than L2 (state {bytes_state / 2**20:.0f} MiB per buffer, "
+                             f"2 buffers)",
+                       "schedule": "recompute" if a.schedule <= 0 else "stash-half2"},
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": bytes_state / e2e_steps,
+                    "d2h_bytes_per_step": bytes_state / e2e_steps,
+                    "call": "osc_set_state(host) + osc_run(Ts=K) + osc_get_state(host)",
+                    "steps": int(summ.iterations), "ms": ms_e2e},
+            "gpu_launches": eng.launches_per_step() * a.steps,
+            "clocks": clocks,
+            "roofline": roof,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    eng.close()
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+def _work_per_cell() -> dict:
+    """Algorithmic FP64 work per beam-step, frozen from ncu (profiles/)."""
+    path = os.path.join(ROOT, "profiles", "fp64_work.json")
+    if os.path.exists(path):
+        return json.load(open(path))
+    # SURVEY.md §8(d) estimate until the ncu measurement is frozen
+    return {"source": "SURVEY.md §8(d) estimate (1.1e3 FP64 instr / beam-step)",
+            "per_stage": {"S2": 1.1e3 * 0.35, "S3": 1.1e3 * 0.3, "S4": 1.1e3 * 0.35}}
+
+
+if __name__ == "__main__":
+    main()

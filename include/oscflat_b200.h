@@ -158,6 +158,13 @@ int osc_debug_sums(OscCtx* ctx, double* out60);
  * 1 = stash half2 in HBM between S3 and S4. */
 int osc_set_schedule(OscCtx* ctx, int schedule);
 
+/* Measured FP64 FMA throughput (thread-level DFMA instructions per second)
+ * from a DFMA-chain microkernel on `device` — the FP64 roofline denominator. */
+int osc_fp64_peak(int device, double* dfma_per_s, double* ms);
+/* Average device time of each stage kernel (S2, S3, S4) over nsteps steps,
+ * bracketed by CUDA events on the context stream (single-GPU contexts). */
+int osc_profile_stages(OscCtx* ctx, int nsteps, float* ms_out3);
+
 /* ---- host-side Environment builder (setup, not the hot path) ----------- */
 /* Mirrors solver::Environment::from_config (solver.cpp:62-95): angle grid,
  * vacuum table, Fermi-Dirac spectra and couplings from physics parameters. */

@@ -118,7 +118,13 @@ class RunConfig:
             if t not in self.provided and e not in self.provided:
                 missing.append(f"{t}|{e}")
         if self.values["hasMatter"]:
-            missing += [k for k in ("Ye",) if k not in self.provided]
+            prof = self.values["matterProfile"]
+            need_m = ["Ye"]
+            if prof in ("exp", "sum"):
+                need_m += ["nb0", "hNS"]
+            if prof in ("powerlaw", "sum"):
+                need_m += ["Mns", "gs", "S"]
+            missing += [k for k in need_m if k not in self.provided]
         if missing:
             raise ConfigError("config leaves required keys uninitialized: " + " ".join(missing))
         v = self.values

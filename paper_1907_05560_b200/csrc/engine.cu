@@ -276,8 +276,19 @@ struct OscCtx {
 
 namespace {
 
-int grid_blocks(OscCtx* c) {
-    return c->nblocks;
+// DFMA-chain microkernel for the FP64 roofline denominator: 8 independent
+// dependency chains per thread keep the FP64 pipe saturated.
+__global__ void k_dfma_peak(double* out, int iters, double y, double z) {
+    double x[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) x[k] = threadIdx.x * 1e-7 + k;
+    for (int i = 0; i < iters; ++i)
+#pragma unroll
+        for (int k = 0; k < 8; ++k) x[k] = fma(x[k], y, z);
+    double s = 0.0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s += x[k];
+    if (s == 12345.678) out[0] = s;  // keep the chains live
 }
 
 void validate(const OscDesc* d) {
@@ -611,6 +622,64 @@ int osc_set_schedule(OscCtx* c, int schedule) {
             cudaGraphExecDestroy(c->graph);
             c->graph = nullptr;
         }
+    });
+}
+
+int osc_fp64_peak(int device, double* dfma_per_s, double* ms_out) {
+    return guarded([&] {
+        CUDA_OK(cudaSetDevice(device));
+        int nsm = 0;
+        CUDA_OK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device));
+        double* d = nullptr;
+        CUDA_OK(cudaMalloc(&d, sizeof(double)));
+        cudaEvent_t e0, e1;
+        CUDA_OK(cudaEventCreate(&e0));
+        CUDA_OK(cudaEventCreate(&e1));
+        const int blocks = nsm * 8, threads = 256, iters = 4096;
+        k_dfma_peak<<<blocks, threads>>>(d, 64, 0.999999, 1e-9);  // warm-up
+        float best = 1e30f;
+        for (int rep = 0; rep < 5; ++rep) {
+            CUDA_OK(cudaEventRecord(e0));
+            k_dfma_peak<<<blocks, threads>>>(d, iters, 0.999999, 1e-9);
+            CUDA_OK(cudaEventRecord(e1));
+            CUDA_OK(cudaEventSynchronize(e1));
+            float ms = 0.f;
+            CUDA_OK(cudaEventElapsedTime(&ms, e0, e1));
+            best = std::min(best, ms);
+        }
+        CUDA_OK(cudaGetLastError());
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        cudaFree(d);
+        *dfma_per_s = (double)blocks * threads * 8.0 * iters / (best * 1e-3);
+        if (ms_out) *ms_out = best;
+    });
+}
+
+int osc_profile_stages(OscCtx* c, int nsteps, float* ms_out) {
+    return guarded([&] {
+        CUDA_OK(cudaSetDevice(c->device));
+        if (c->nranks != 1) throw Error(OSC_ERR_CONFIG, "osc_profile_stages: single-GPU contexts only");
+        cudaEvent_t ev[4];
+        for (auto& e : ev) CUDA_OK(cudaEventCreate(&e));
+        double acc[3] = {0, 0, 0};
+        for (int i = 0; i < nsteps; ++i) {
+            CUDA_OK(cudaEventRecord(ev[0], c->stream));
+            c->launch_stage(2);
+            CUDA_OK(cudaEventRecord(ev[1], c->stream));
+            c->launch_stage(3);
+            CUDA_OK(cudaEventRecord(ev[2], c->stream));
+            c->launch_stage(4);
+            CUDA_OK(cudaEventRecord(ev[3], c->stream));
+            CUDA_OK(cudaEventSynchronize(ev[3]));
+            for (int k = 0; k < 3; ++k) {
+                float ms = 0.f;
+                CUDA_OK(cudaEventElapsedTime(&ms, ev[k], ev[k + 1]));
+                acc[k] += ms;
+            }
+        }
+        for (auto& e : ev) cudaEventDestroy(e);
+        for (int k = 0; k < 3; ++k) ms_out[k] = (float)(acc[k] / std::max(1, nsteps));
     });
 }
 

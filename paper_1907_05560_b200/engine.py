@@ -250,8 +250,20 @@ class Engine:
         check(lib().osc_debug_sums(self._ctx, out.ctypes.data_as(C.POINTER(C.c_double))))
         return out.reshape(5, 12)
 
+    def profile_stages(self, nsteps: int) -> list:
+        out = (C.c_float * 3)()
+        check(lib().osc_profile_stages(self._ctx, nsteps, out))
+        return [float(x) for x in out]
+
     def set_schedule(self, schedule: int) -> None:
         check(lib().osc_set_schedule(self._ctx, schedule))
+
+
+def fp64_peak(device: int = 0) -> float:
+    """Thread-level DFMA instructions per second measured on `device`."""
+    v, ms = C.c_double(), C.c_double()
+    check(lib().osc_fp64_peak(device, C.byref(v), C.byref(ms)))
+    return v.value
 
 
 def comm_unique_id() -> bytes:
@@ -264,7 +276,7 @@ def fermi_integral(k: int, eta: float) -> float:
     return lib().osc_fermi_integral(k, eta)
 
 
-ConfigError = native.ConfigError
+ConfigError = native._ConfigErrorBase  # base of native.ConfigError and config errors
 NumericError = native.NumericError
 IoError = native.IoError
 ParallelError = native.ParallelError

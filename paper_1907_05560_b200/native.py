@@ -9,6 +9,7 @@ import ctypes as C
 import os
 
 from .build import LIB
+from .config import ConfigError as _ConfigErrorBase
 
 _dp = C.POINTER(C.c_double)
 
@@ -67,7 +68,7 @@ SYMBOLS = [
     "osc_set_state_device", "osc_get_state_device", "osc_trial_step_error", "osc_run",
     "osc_max_norm_dev", "osc_begin", "osc_enqueue_steps", "osc_query", "osc_synchronize",
     "osc_stream", "osc_launches_per_step", "osc_debug_sums", "osc_set_schedule",
-    "osc_env_build", "osc_env_desc", "osc_env_destroy", "osc_fermi_integral",
+    "osc_fp64_peak", "osc_profile_stages", "osc_env_build", "osc_env_desc", "osc_env_destroy", "osc_fermi_integral",
 ]
 
 _lib = None
@@ -104,6 +105,8 @@ def lib() -> C.CDLL:
     L.osc_launches_per_step.argtypes = [vp]
     L.osc_debug_sums.argtypes = [vp, _dp]
     L.osc_set_schedule.argtypes = [vp, C.c_int]
+    L.osc_fp64_peak.argtypes = [C.c_int, _dp, _dp]
+    L.osc_profile_stages.argtypes = [vp, C.c_int, C.POINTER(C.c_float)]
     L.osc_env_build.argtypes = [C.POINTER(OscParams), C.POINTER(vp)]
     L.osc_env_desc.argtypes = [vp, C.POINTER(OscDesc), _dp]
     L.osc_env_destroy.argtypes = [vp]
@@ -119,7 +122,7 @@ class OscError(RuntimeError):
     status = 0
 
 
-class ConfigError(OscError):
+class ConfigError(OscError, _ConfigErrorBase):
     status = 1
 
 

@@ -1,0 +1,315 @@
+"""GPU parity tests: the CUDA path (through the C-ABI) against the reference.
+
+Oracles: golden fixtures produced by the unmodified reference
+(tests/golden/), the compiled reference itself (oracle/_ref) and the C
+restatement (oracle/oscflat_oracle.c).  Tolerances follow BASELINE.json's
+north star: every rho component within 1e-8, trace conserved to 1e-12 — in
+resolved windows.  The integrator scenarios restate the
+reference's test_solver.cpp.
+"""
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+from paper_1907_05560_b200 import (Engine, Environment, NumericError, StepControl,
+                                   baseline_config, parse_config)
+
+pytestmark = pytest.mark.gpu
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+RHO_TOL = 1e-8     # north star: max |d rho| per component
+TRACE_TOL = 1e-12  # north star: |trace - 1|
+
+
+def rho(state):
+    """mode-1 payload -> (|a|^2-|b|^2, 2Re ab*, 2Im ab*, trace) per bin."""
+    s = state.reshape(-1, 4, 4, state.shape[-1] if state.ndim > 1 else 1)
+    return s
+
+
+def density(mode1, ebins):
+    s = mode1.reshape(-1, 4, 4, ebins)  # [traj][species][comp][e]
+    ar, ai, br, bi = s[:, :, 0], s[:, :, 1], s[:, :, 2], s[:, :, 3]
+    return np.stack([ar * ar + ai * ai - br * br - bi * bi, 2 * (ar * br + ai * bi),
+                     2 * (ai * br - ar * bi)]), ar * ar + ai * ai + br * br + bi * bi
+
+
+def make(cfg):
+    env = Environment.from_config(cfg)
+    eng = Engine(env)
+    eng.init_states()
+    return env, eng
+
+
+@pytest.fixture(scope="module")
+def golden():
+    return np.load(os.path.join(GOLD, "golden.npz"))
+
+
+@pytest.fixture(scope="module")
+def cases():
+    meta = json.load(open(os.path.join(GOLD, "golden_meta.json")))
+    return {k: parse_config(v) for k, v in meta["cases"].items()}
+
+
+NAMES = ["bulb_resolved", "bulb_unresolved", "ebulb_resolved", "sa_resolved",
+         "bulb_adaptive_matter"]
+
+
+@pytest.mark.parametrize("name", NAMES)
+def test_init_states_bit_exact(golden, cases, name):
+    env, eng = make(cases[name])
+    got = eng.state()
+    want = golden[f"{name}/init_state"]
+    assert np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("name", NAMES)
+def test_trial_step_error_matches_reference(golden, cases, name):
+    cfg = cases[name]
+    env, eng = make(cfg)
+    err = eng.trial_step_error(cfg.values["R0"], cfg.values["dr"])
+    assert err == pytest.approx(golden[f"{name}/trial_err"][0], rel=1e-7)
+
+
+@pytest.mark.parametrize("name", NAMES)
+def test_run_matches_reference_golden(golden, cases, name):
+    cfg = cases[name]
+    env, eng = make(cfg)
+    s = eng.run(StepControl.from_config(cfg))
+    summ = golden[f"{name}/summary"]
+    assert (s.iterations, s.accepted, s.rejected) == tuple(int(x) for x in summ[1:4])
+    assert s.final_r == pytest.approx(summ[0], rel=1e-14)
+    got, want = eng.state(), golden[f"{name}/final_state"]
+    (rg, tg), (rw, tw) = density(got, env.ebins), density(want, env.ebins)
+    if "unresolved" in name:
+        # literal configs[0] step at 10 km: lambda*dl ~ 4e4 rad, ill-conditioned
+        # even reference-vs-reference
+        assert np.max(np.abs(rg - rw)) <= 1e-5
+    else:
+        assert np.max(np.abs(rg - rw)) <= RHO_TOL * 1e-3
+        assert np.max(np.abs(got - want)) <= 1e-12
+        assert np.max(np.abs(tg - 1.0)) <= TRACE_TOL
+
+
+def test_configs0_shape_resolved_window_vs_oracle(pyoracle):
+    """configs[0] shape (256 x 100 bulb) in a resolved window: rho within 1e-8
+    of the C oracle, trace within 1e-12 (BASELINE.md parity window)."""
+    cfg = baseline_config("configs0", R0=50, Rn=60, dr=5e-5, max_dr=5e-5, Ts=200)
+    env, eng = make(cfg)
+    s = eng.run(StepControl.from_config(cfg))
+    o = pyoracle.Oracle(cfg)
+    so = o.run()
+    assert s.iterations == so["iterations"] == 200
+    (rg, tg), (ro, to) = density(eng.state(), env.ebins), density(o.get_state(), env.ebins)
+    assert np.max(np.abs(rg - ro)) <= RHO_TOL
+    assert np.max(np.abs(tg - 1.0)) <= TRACE_TOL
+    assert s.final_max_norm_dev <= TRACE_TOL
+
+
+def test_configs0_shape_vs_compiled_reference(ref):
+    """Same window, against the unmodified reference engine on all host cores."""
+    cfg = baseline_config("configs0", R0=50, Rn=60, dr=5e-5, max_dr=5e-5, Ts=100)
+    env, eng = make(cfg)
+    eng.run(StepControl.from_config(cfg))
+    want, summ = ref.run(cfg.render(), lanes=min(os.cpu_count() or 1, 16))
+    (rg, _), (rw, _) = density(eng.state(), env.ebins), density(want, env.ebins)
+    assert summ["iterations"] == 100
+    assert np.max(np.abs(rg - rw)) <= RHO_TOL
+
+
+def test_ebulb_symmetry_breaking_vs_oracle(pyoracle):
+    cfg = baseline_config("configs0", Abins=32, Ebins=24, R0=50, Rn=60, dr=5e-5, max_dr=5e-5,
+                          Ts=60)
+    cfg.override("model=ebulb").override("Pbins=16").override("perturb=1e-8")
+    env, eng = make(cfg)
+    eng.run(StepControl.from_config(cfg))
+    o = pyoracle.Oracle(cfg)
+    o.run()
+    (rg, tg), (ro, _) = density(eng.state(), env.ebins), density(o.get_state(), env.ebins)
+    assert np.max(np.abs(rg - ro)) <= RHO_TOL
+    assert np.max(np.abs(tg - 1.0)) <= TRACE_TOL
+
+
+def test_full_size_configs2_properties():
+    """configs[2] at full size (4096 x 256, 1M beams): size-independent
+    properties — unitarity, determinism, schedule invariance, state round trip."""
+    cfg = baseline_config("configs2", R0=50, Rn=60, dr=5e-5, max_dr=5e-5, Ts=20)
+    env, eng = make(cfg)
+    s0 = eng.state()
+    eng.set_state(s0)
+    assert np.array_equal(eng.state(), s0)  # mode-1 round trip
+    s = eng.run(StepControl.from_config(cfg))
+    a = eng.state()
+    assert s.iterations == 20 and s.final_max_norm_dev <= TRACE_TOL
+    eng.set_state(s0)
+    eng.set_schedule(1)  # stash half2 instead of recomputing it
+    eng.run(StepControl.from_config(cfg))
+    assert np.array_equal(eng.state(), a)  # bitwise: same arithmetic, same order
+    eng.set_state(s0)
+    eng.set_schedule(0)
+    eng.run(StepControl.from_config(cfg))
+    assert np.array_equal(eng.state(), a)  # deterministic reductions
+    _, t = density(a, env.ebins)
+    assert np.max(np.abs(t - 1.0)) <= TRACE_TOL
+
+
+# ---------------------------------------------------- test_solver.cpp restated
+def base_config():
+    return parse_config(
+        "dm2= -3e-3\ntheta= 0.1\nR0= 60\nRn= 70\ndr= 1e-2\nmax_dr= 1.0\n"
+        "E0= 0\nE1= 80\nAbins= 4\nPbins= 1\nEbins= 8\neps0= 1e-8\nkappa= 0.8\n"
+        "Rv= 10\nmodel= bulb\nhasMatter= 0\n"
+        "Lve= 0\nLvae= 0\nLvt= 0\nLvat= 0\n"
+        "Eve= 11\nEvae= 16\nEvt= 25\nEvat= 25\n"
+        "eta_ve= 3\neta_vae= 3\neta_vt= 3\neta_vat= 3\n")
+
+
+def test_embedded_error_is_third_order():
+    env, eng = make(base_config())
+    drs, errs = [], []
+    dr = 2.0
+    for _ in range(5):
+        e = eng.trial_step_error(60.0, dr)
+        assert e > 0
+        drs.append(math.log(dr))
+        errs.append(math.log(e))
+        dr *= 0.5
+    slope = np.polyfit(drs, errs, 1)[0]
+    assert 2.5 <= slope <= 3.5
+
+
+def test_trial_steps_never_mutate_state():
+    env, eng = make(base_config())
+    before = eng.state()
+    eng.trial_step_error(60.0, 0.5)
+    eng.trial_step_error(60.0, 0.25)
+    assert np.array_equal(eng.state(), before)
+
+
+def test_rn_equal_r0_terminates_immediately():
+    cfg = base_config().override("Rn=60")
+    env, eng = make(cfg)
+    s = eng.run(StepControl.from_config(cfg))
+    assert s.iterations == 0 and s.final_r == 60.0 and s.termination == "radius"
+
+
+def test_ts_caps_iterations():
+    cfg = base_config().override("Ts=100").override("Rn=1000").override("max_dr=1e-2")
+    env, eng = make(cfg)
+    s = eng.run(StepControl.from_config(cfg))
+    assert s.iterations == 100 and s.accepted + s.rejected == 100
+    assert s.termination == "iterations"
+
+
+def test_infinite_tolerance_walks_at_max_dr():
+    cfg = base_config().override("eps0=1e30").override("max_dr=0.5").override("Rn=70")
+    env, eng = make(cfg)
+    s = eng.run(StepControl.from_config(cfg))
+    assert s.rejected == 0 and s.final_r == pytest.approx(70.0)
+    assert abs(s.iterations - 21) <= 4
+
+
+def test_adaptive_run_matches_oracle_accept_reject_sequence(pyoracle):
+    cfg = base_config().override("Lve=1e51").override("Lvae=1e51").override("Lvt=1e51")
+    cfg.override("Lvat=1e51").override("Abins=8").override("R0=50").override("Rn=55")
+    cfg.override("Ts=150")
+    env, eng = make(cfg)
+    s = eng.run(StepControl.from_config(cfg))
+    o = pyoracle.Oracle(cfg)
+    so = o.run()
+    assert (s.accepted, s.rejected) == (so["accepted"], so["rejected"])
+    assert s.final_r == pytest.approx(so["final_r"], rel=1e-12)
+    assert np.max(np.abs(eng.state() - o.get_state())) <= 1e-10
+    assert s.final_max_norm_dev <= 1e-10  # collective run unitarity (test_solver.cpp:208-224)
+
+
+def test_tiny_tolerance_collapses_with_numeric_error():
+    cfg = base_config().override("eps0=1e-280").override("min_dr=1e-6")
+    env, eng = make(cfg)
+    with pytest.raises(NumericError):
+        eng.run(StepControl.from_config(cfg))
+
+
+def test_single_angle_vacuum_closed_form():
+    cfg = base_config().override("model=sa").override("Abins=1").override("R0=50")
+    cfg.override("Rn=250").override("Ebins=16")
+    env, eng = make(cfg)
+    s = eng.run(StepControl.from_config(cfg))
+    assert s.final_r == pytest.approx(250.0)
+    st = eng.state().reshape(1, 4, 4, 16)
+    L = 200.0
+    for e in range(16):
+        E = (e + 0.5) * 80.0 / 16.0
+        delta = (-3e-3 * 1e-12 / (2 * E)) / 197.327e-18
+        want = 1 - np.sin(0.2) ** 2 * np.sin(0.5 * delta * L) ** 2
+        got = st[0, 0, 0, e] ** 2 + st[0, 0, 1, e] ** 2
+        assert got == pytest.approx(want, rel=1e-8)
+    assert s.final_max_norm_dev <= 1e-11
+
+
+def test_constant_matter_matches_series_exponential():
+    cfg = base_config()
+    for kv in ("model=sa", "Abins=1", "R0=15", "Rn=15.5", "max_dr=0.01", "hasMatter=1",
+               "matterProfile=exp", "Ye=0.4", "nb0=1e30", "hNS=1e15", "Ebins=4"):
+        cfg.override(kv)
+    env, eng = make(cfg)
+    eng.run(StepControl.from_config(cfg))
+    st = eng.state().reshape(1, 4, 4, 4)
+    hc = 197.327e-13
+    A = (math.sqrt(2) * 1.166e-11 * 0.4 * 1e30 * math.exp(-(15 - 10) / 1e15) * hc ** 3) / 197.327e-18
+    t = env.tables()
+    import scipy.linalg as sl
+
+    for sp in (0, 1):
+        for e in range(4):
+            sgn = -1.0 if sp == 1 else 1.0
+            h11 = t["vac11"][e] + sgn * 0.5 * A
+            h12 = t["vac12"][e]
+            H = np.array([[h11, h12], [h12, -h11]], dtype=complex)
+            U = sl.expm(-1j * 0.5 * H)
+            psi = U @ np.array([1.0, 0.0] if sp < 2 else [0.0, 1.0])
+            want = [psi[0].real, psi[0].imag, psi[1].real, psi[1].imag]
+            np.testing.assert_allclose(st[0, sp, :, e], want, atol=1e-9)
+
+
+def test_run_dump_resume_is_bit_exact():
+    cfg = base_config()
+    for kv in ("Lve=1e51", "Lvae=1e51", "Lvt=1e51", "Lvat=1e51", "Abins=6", "R0=50", "Rn=53"):
+        cfg.override(kv)
+    env, eng = make(cfg)
+    snaps = []
+
+    def hook(info, state):
+        if info.iter % 8 == 0:
+            snaps.append((info, state))
+
+    eng.run(StepControl.from_config(cfg), hook)
+    final = eng.state()
+    assert len(snaps) >= 2
+    info, state = snaps[1]
+    env2, eng2 = make(cfg)
+    eng2.set_state(state)
+    ctl = StepControl.from_config(cfg)
+    ctl.r, ctl.dr, ctl.iter = info.r, info.dr, info.iter
+    eng2.run(ctl)
+    assert np.array_equal(eng2.state(), final)
+
+
+def test_non_finite_state_raises_numeric_error():
+    env, eng = make(base_config())
+    s = eng.state()
+    s[5] = np.nan
+    eng.set_state(s)
+    with pytest.raises(NumericError):
+        eng.run(StepControl.from_config(base_config()))
+
+
+def test_state_size_mismatch_is_io_error():
+    from paper_1907_05560_b200 import IoError
+
+    env, eng = make(base_config())
+    with pytest.raises(IoError):
+        eng.set_state(np.zeros(7))
