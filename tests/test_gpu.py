@@ -91,7 +91,11 @@ def test_run_matches_reference_golden(golden, cases, name):
     else:
         assert np.max(np.abs(rg - rw)) <= RHO_TOL * 1e-3
         assert np.max(np.abs(got - want)) <= 1e-12
-        assert np.max(np.abs(tg - 1.0)) <= TRACE_TOL
+        # the averaged pair (solver.cpp:404-409) is not exactly norm preserving:
+        # trace must track the reference's own trace, and stay within 1e-12 of
+        # one wherever the reference does
+        assert np.max(np.abs(tg - tw)) <= 1e-13
+        assert np.max(np.abs(tg - 1.0)) <= max(TRACE_TOL, np.max(np.abs(tw - 1.0)) + 1e-13)
 
 
 def test_configs0_shape_resolved_window_vs_oracle(pyoracle):
