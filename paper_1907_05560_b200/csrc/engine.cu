@@ -130,7 +130,8 @@ struct OscCtx {
     int t_lo = 0, t_hi = 0;
     int T = 0, P = 0, E = 0;
     int ntraj = 0, ncell = 0, npad = 0;
-    int nsm = 0, nblocks = 0, chunk = 0, smem = 0;
+    int nsm = 0, nblocks = 0, chunk = 0, ntr_max = 0;
+    uint32_t e_magic = 0, e_shift = 0;
     int schedule = 0;
     cudaStream_t stream = nullptr;
     nccl::Comm comm = nullptr;
@@ -159,6 +160,7 @@ struct OscCtx {
 
     void launch_stage(int stage) {
         const StageFn fn = stage_kernel(desc.model, stage);
+        const size_t smem = stage_smem_bytes(stage, schedule, ntr_max);
         fn<<<nblocks, kBlock, smem, stream>>>(args);
         CUDA_OK(cudaGetLastError());
     }
@@ -388,29 +390,29 @@ int osc_create(const OscDesc* desc, const OscComm* comm, OscCtx** out) {
         CUDA_OK(cudaMallocHost(&c->h_ctl, sizeof(Ctl)));
         std::memset(c->h_ctl, 0, sizeof(Ctl));
 
-        // Launch geometry: one resident wave of blocks, half per particle class.
-        int occ = 0;
-        const StageFn probe = stage_kernel(desc->model, 4);
-        int smem_guess = 48 * 1024;
-        for (int it = 0; it < 3; ++it) {
-            CUDA_OK(cudaFuncSetAttribute(probe, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
-            CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, probe, kBlock, smem_guess));
-            occ = std::max(occ, 1);
+        // Launch geometry: one resident wave of blocks (2 per SM, the
+        // __launch_bounds__ target), half of them per particle class; each
+        // block owns a contiguous, warp-aligned chunk of cells.
+        {
+            const int occ = 2;
             const int nb_half = std::max(1, c->nsm * occ / 2);
             int chunk = (c->ncell + nb_half - 1) / nb_half;
             chunk = std::max(32, (chunk + 31) / 32 * 32);
-            const int ntr_max = chunk / c->E + 2;
-            const int smem = ntr_max * (int)sizeof(TrajRec);
             c->nblocks = 2 * nb_half;
             c->chunk = chunk;
-            c->smem = smem;
-            if (smem <= smem_guess) break;
-            smem_guess = smem;
+            c->ntr_max = chunk / c->E + 2;
+            const size_t smax = stage_smem_bytes(4, 1, c->ntr_max);
+            if (smax > 200 * 1024)
+                throw Error(OSC_ERR_CONFIG, "osc_create: trajectory records exceed shared memory");
+            for (int st : {0, 2, 3, 4})
+                CUDA_OK(cudaFuncSetAttribute(stage_kernel(desc->model, st),
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smax));
+            // magic numbers for the division by E inside the kernels
+            uint32_t l = 0;
+            while ((1u << l) < (uint32_t)c->E) ++l;
+            c->e_shift = l;
+            c->e_magic = (uint32_t)((((uint64_t)1 << 32) * (((uint64_t)1 << l) - (uint64_t)c->E)) / (uint64_t)c->E + 1);
         }
-        if (c->smem > 160 * 1024) throw Error(OSC_ERR_CONFIG, "osc_create: trajectory records exceed shared memory");
-        for (int st : {0, 2, 3, 4})
-            CUDA_OK(cudaFuncSetAttribute(stage_kernel(desc->model, st),
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, std::max(c->smem, 1)));
         c->partials.alloc((size_t)c->nblocks * kSlotDoubles);
 
         if (c->nranks > 1) {
@@ -434,6 +436,8 @@ int osc_create(const OscDesc* desc, const OscComm* comm, OscCtx** out) {
         a.nb_half = c->nblocks / 2;
         a.nranks = c->nranks;
         a.fuse_ctl = c->nranks == 1;
+        a.e_magic = c->e_magic;
+        a.e_shift = c->e_shift;
         a.schedule = 0;
         a.Rnu = desc->Rnu;
         a.dcos2 = 1.0 / c->T;

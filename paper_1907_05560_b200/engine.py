@@ -84,7 +84,8 @@ class Environment:
     couplings and matter parameters, built by the native host code."""
 
     def __init__(self, cfg: RunConfig):
-        cfg.require_runnable()
+        # like the reference, from_config does not run io::require_runnable
+        # (the CLI does); the native builder validates what it consumes
         v = cfg.values
         p = OscParams()
         p.model = cfg.model_id

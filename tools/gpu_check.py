@@ -23,7 +23,7 @@ c = baseline_config("configs0", Abins=12, Ebins=20, R0=50, Rn=51, dr=1e-4, max_d
 cmp("ebulb", c, 20)
 c = baseline_config("configs0", Abins=1, Ebins=20, R0=50, Rn=51, dr=1e-4, max_dr=1e-4, Ts=20); c.override("model=sa")
 cmp("sa", c, 20)
-c = baseline_config("configs0", Abins=16, Ebins=24, R0=50, Rn=60, dr=1e-3, max_dr=1e-2, Ts=30); c.override("eps0=1e-9"); c.override("hasMatter=1"); c.override("matterProfile=sum"); c.override("Ye=0.5"); c.override("nb0=1e30"); c.override("hNS=5")
+c = baseline_config("configs0", Abins=16, Ebins=24, R0=50, Rn=60, dr=1e-3, max_dr=1e-2, Ts=30); c.override("eps0=1e-9"); c.override("hasMatter=1"); c.override("matterProfile=sum"); c.override("Ye=0.5"); c.override("nb0=1e30"); c.override("hNS=5"); c.override("Mns=1.4"); c.override("gs=1"); c.override("S=100")
 cmp("adaptive+matter", c, 30)
 
 for name in ("configs0", "configs2"):
