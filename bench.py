@@ -306,7 +306,7 @@ def main():
                        "parallelism": f"theta-sharded x{world}",
                        "l2": f"inputs larger than L2 (state {bytes_state / 2**20:.0f} MiB per buffer, "
                              f"2 buffers)",
-                       "schedule": "recompute" if a.schedule <= 0 else "stash-half2"},
+                       "schedule": "recompute" if a.schedule == 0 else "stash-half2"},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": bytes_state / e2e_steps,
                     "d2h_bytes_per_step": bytes_state / e2e_steps,
                     "call": "osc_set_state(host) + osc_run(Ts=K) + osc_get_state(host)",

@@ -32,21 +32,25 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, out: str | None = None,
+          defines: tuple = ()) -> str:
+    """Compile to ``out`` (default: the in-tree ``_oscb200.so``).  ``defines``
+    are extra -D tuning knobs (e.g. OSC_MIN_BLOCKS=3) for variant sweeps."""
+    target = out or LIB
+    if target == LIB and not defines and not force and not _stale():
         return LIB
-    cmd = [NVCC, *ARCH, *FLAGS, "-I", os.path.join(ROOT, "include"), "-I", CSRC,
-           *[os.path.join(CSRC, s) for s in SOURCES], "-o", LIB + ".tmp", "-ldl"]
-    out = subprocess.run(cmd, capture_output=True, text=True)
+    cmd = [NVCC, *ARCH, *FLAGS, *[f"-D{d}" for d in defines], "-I", os.path.join(ROOT, "include"),
+           "-I", CSRC, *[os.path.join(CSRC, s) for s in SOURCES], "-o", target + ".tmp", "-ldl"]
+    res = subprocess.run(cmd, capture_output=True, text=True)
     log = os.path.join(PKG, "_build.log")
     with open(log, "w") as f:
-        f.write(" ".join(cmd) + "\n" + out.stdout + out.stderr)
-    if out.returncode != 0:
-        raise RuntimeError("nvcc failed:\n" + out.stderr[-6000:])
-    os.replace(LIB + ".tmp", LIB)
+        f.write(" ".join(cmd) + "\n" + res.stdout + res.stderr)
+    if res.returncode != 0:
+        raise RuntimeError("nvcc failed:\n" + res.stderr[-6000:])
+    os.replace(target + ".tmp", target)
     if verbose:
-        print(out.stderr)
-    return LIB
+        print(res.stderr)
+    return target
 
 
 if __name__ == "__main__":

@@ -132,7 +132,8 @@ struct OscCtx {
     int ntraj = 0, ncell = 0, npad = 0;
     int nsm = 0, nblocks = 0, chunk = 0, ntr_max = 0;
     uint32_t e_magic = 0, e_shift = 0;
-    int schedule = 0;
+    int schedule = 1;  // 1: stash half2 (default), 0: recompute it in S4
+    int use_pdl = 1;
     cudaStream_t stream = nullptr;
     nccl::Comm comm = nullptr;
 
@@ -158,11 +159,22 @@ struct OscCtx {
         if (stream) cudaStreamDestroy(stream);
     }
 
+    // Stage kernels are launched with programmatic dependent launch so each
+    // one is scheduled while its predecessor drains (griddepcontrol in the
+    // kernels orders the dependent reads).
     void launch_stage(int stage) {
         const StageFn fn = stage_kernel(desc.model, stage);
-        const size_t smem = stage_smem_bytes(stage, schedule, ntr_max);
-        fn<<<nblocks, kBlock, smem, stream>>>(args);
-        CUDA_OK(cudaGetLastError());
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(nblocks);
+        cfg.blockDim = dim3(kBlock);
+        cfg.dynamicSmemBytes = stage_smem_bytes(stage, schedule, ntr_max);
+        cfg.stream = stream;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = use_pdl ? 1 : 0;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        CUDA_OK(cudaLaunchKernelEx(&cfg, fn, args));
     }
 
     void exchange(int slot) {
@@ -183,7 +195,7 @@ struct OscCtx {
         launch_stage(4);
         exchange(3);
         if (nranks > 1) {
-            k_control<<<1, 32, 0, stream>>>(args);
+            k_control<<<1, 128, 0, stream>>>(args);
             CUDA_OK(cudaGetLastError());
         }
     }
@@ -254,6 +266,7 @@ struct OscCtx {
         h.accepted = h.rejected = 0;
         h.err = 0.0;
         h.status = h.reason = 0;
+        h.bad_sums = 0;
         h.commit = commit;
         h.dr_max = c.dr_max;
         h.dr_min = c.dr_min;
@@ -394,11 +407,11 @@ int osc_create(const OscDesc* desc, const OscComm* comm, OscCtx** out) {
         // __launch_bounds__ target), half of them per particle class; each
         // block owns a contiguous, warp-aligned chunk of cells.
         {
-            const int occ = 2;
-            const int nb_half = std::max(1, c->nsm * occ / 2);
-            int chunk = (c->ncell + nb_half - 1) / nb_half;
+            const int occ = OSC_MIN_BLOCKS;
+            const int nb = std::max(1, c->nsm * occ);
+            int chunk = (c->ncell + nb - 1) / nb;
             chunk = std::max(32, (chunk + 31) / 32 * 32);
-            c->nblocks = 2 * nb_half;
+            c->nblocks = nb;
             c->chunk = chunk;
             c->ntr_max = chunk / c->E + 2;
             const size_t smax = stage_smem_bytes(4, 1, c->ntr_max);
@@ -433,12 +446,12 @@ int osc_create(const OscDesc* desc, const OscComm* comm, OscCtx** out) {
         a.ncell = c->ncell;
         a.npad = c->npad;
         a.chunk = c->chunk;
-        a.nb_half = c->nblocks / 2;
         a.nranks = c->nranks;
         a.fuse_ctl = c->nranks == 1;
         a.e_magic = c->e_magic;
         a.e_shift = c->e_shift;
-        a.schedule = 0;
+        a.schedule = c->schedule;
+        c->half2.alloc((size_t)c->npad * 16);
         a.Rnu = desc->Rnu;
         a.dcos2 = 1.0 / c->T;
         a.phi_measure = desc->model == OSC_MODEL_EXT_BULB ? 1.0 / c->P : 1.0;
@@ -458,7 +471,7 @@ int osc_create(const OscDesc* desc, const OscComm* comm, OscCtx** out) {
         a.S = desc->S;
         a.psi0_buf[0] = c->psi[0].p;
         a.psi0_buf[1] = c->psi[1].p;
-        a.half2 = nullptr;
+        a.half2 = c->half2.p;
         a.xbuf = c->xbuf.p;
         a.xsend = c->nranks > 1 ? c->xsend.p : c->xbuf.p;
         a.partials = c->partials.p;

@@ -79,9 +79,10 @@ def lib() -> C.CDLL:
     global _lib
     if _lib is not None:
         return _lib
-    if not os.path.exists(LIB):
-        raise RuntimeError(f"native library {LIB} is missing; run __graft_entry__.build()")
-    L = C.CDLL(LIB, mode=C.RTLD_GLOBAL)
+    path = os.environ.get("OSC_LIB", LIB)  # variant sweeps (tools/) may point elsewhere
+    if not os.path.exists(path):
+        raise RuntimeError(f"native library {path} is missing; run __graft_entry__.build()")
+    L = C.CDLL(path, mode=C.RTLD_GLOBAL)
     vp = C.c_void_p
     L.osc_last_error.restype = C.c_char_p
     L.osc_comm_unique_id.argtypes = [vp]
