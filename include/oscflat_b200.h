@@ -40,8 +40,16 @@ typedef enum {
     OSC_ERR_CUDA = 5      /* device / driver failure (no reference analogue) */
 } OscStatus;
 
-/* geom::Model (geometry.hpp:11) */
-enum { OSC_MODEL_SINGLE_ANGLE = 0, OSC_MODEL_BULB = 1, OSC_MODEL_EXT_BULB = 2 };
+/* geom::Model (geometry.hpp:11), extended with the plane (BASELINE configs[3],
+ * paper Eq. 3.19) and cylinder (configs[4], Eq. 3.20) geometries, which the
+ * reference does not implement. */
+enum {
+    OSC_MODEL_SINGLE_ANGLE = 0,
+    OSC_MODEL_BULB = 1,
+    OSC_MODEL_EXT_BULB = 2,
+    OSC_MODEL_PLANE = 3,
+    OSC_MODEL_CYLINDER = 4
+};
 /* matter::Profile (matter.hpp:9) */
 enum { OSC_MATTER_POWERLAW = 0, OSC_MATTER_EXP = 1, OSC_MATTER_SUM = 2, OSC_MATTER_OFF = 3 };
 
@@ -52,10 +60,14 @@ typedef struct OscDesc {
     int abins, pbins;   /* AngleGrid::abins / pbins (geometry.hpp:24-36)      */
     int ebins;          /* logical energy bins                                */
     double Rnu;         /* km                                                 */
-    const double* cos2_theta0; /* [abins]  AngleGrid::cos2_theta0             */
-    const double* sin_theta0;  /* [abins]  AngleGrid::sin_theta0              */
-    const double* cos_phi;     /* [pbins]  AngleGrid::cos_phi                 */
-    const double* sin_phi;     /* [pbins]  AngleGrid::sin_phi                 */
+    /* angle tables; models 0-2: AngleGrid::cos2_theta0 / sin_theta0 /
+     * cos_phi / sin_phi.  Plane: cos(theta), sin(theta) of the zenith bins
+     * and cos/sin(phi).  Cylinder: cos(a0), sin(a0) of the in-plane emission
+     * angle and cos(b), sin(b) of the axial tilt. */
+    const double* cos2_theta0; /* [abins] */
+    const double* sin_theta0;  /* [abins] */
+    const double* cos_phi;     /* [pbins] */
+    const double* sin_phi;     /* [pbins] */
     const double* vac_h11;     /* [ebins]  VacuumTable::h11 (geometry.hpp:118)*/
     const double* vac_h12;     /* [ebins]  VacuumTable::h12                   */
     const double* fw;          /* [4][ebins] SpectrumTable::weights() f*dE    */

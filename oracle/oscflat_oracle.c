@@ -105,15 +105,31 @@ int orc_env_create(const OrcParams* p, OrcEnv** out) {
     v->sin0 = malloc(sizeof(double) * v->T);
     v->cphi = malloc(sizeof(double) * v->P);
     v->sphi = malloc(sizeof(double) * v->P);
-    for (int t = 0; t < v->T; ++t) { /* geometry.cpp:52-55 */
-        v->cos2[t] = (t + 0.5) / v->T;
-        v->sin0[t] = sqrt(1.0 - v->cos2[t]);
-    }
-    const double dphi = 2.0 * K_PI / v->P;
-    for (int q = 0; q < v->P; ++q) {
-        const double phi = (q + 0.5) * dphi;
-        v->cphi[q] = cos(phi);
-        v->sphi[q] = sin(phi);
+    if (v->model == ORC_CYLINDER) {
+        /* in-plane emission angle a0 uniform on (-pi/2, pi/2); axial tilt b
+         * uniform in sin(b) on (-1, 1): tables carry cos/sin of each */
+        for (int t = 0; t < v->T; ++t) {
+            const double a0 = -0.5 * K_PI + (t + 0.5) * K_PI / v->T;
+            v->cos2[t] = cos(a0);
+            v->sin0[t] = sin(a0);
+        }
+        for (int q = 0; q < v->P; ++q) {
+            const double sb = -1.0 + (q + 0.5) * 2.0 / v->P;
+            v->sphi[q] = sb;
+            v->cphi[q] = sqrt(1.0 - sb * sb);
+        }
+    } else {
+        for (int t = 0; t < v->T; ++t) { /* geometry.cpp:52-55; plane: cos(theta) midpoints */
+            const double u = (t + 0.5) / v->T;
+            v->cos2[t] = u;
+            v->sin0[t] = (v->model == ORC_PLANE) ? sqrt(1.0 - u * u) : sqrt(1.0 - u);
+        }
+        const double dphi = 2.0 * K_PI / v->P;
+        for (int q = 0; q < v->P; ++q) {
+            const double phi = (q + 0.5) * dphi;
+            v->cphi[q] = cos(phi);
+            v->sphi[q] = sin(phi);
+        }
     }
     /* VacuumTable::make, geometry.cpp:218-240 */
     v->vac11 = malloc(sizeof(double) * v->E);
@@ -273,6 +289,7 @@ struct OrcEngine {
     size_t nbeam;          /* doubles per set: ntraj*4*4*E */
     double* set[S_NSETS];
     CacheRow* cache[3];    /* [abins] each, local range filled */
+    double* dlj[3];        /* [local traj] dl slots (per trajectory) */
     double r, dr, A[3];
     double sums[4][12];    /* sums0..sums3 totals */
     double (*hvvA)[3], (*hvvB)[3], (*hvvC)[3];
@@ -306,6 +323,7 @@ int orc_engine_create(const OrcEnv* env, int t_lo, int t_hi, OrcEngine** out) {
     g->nbeam = (size_t)g->ntraj * 16 * env->E;
     for (int k = 0; k < S_NSETS; ++k) g->set[k] = calloc(g->nbeam ? g->nbeam : 1, sizeof(double));
     for (int k = 0; k < 3; ++k) g->cache[k] = calloc(env->T, sizeof(CacheRow));
+    for (int k = 0; k < 3; ++k) g->dlj[k] = calloc(g->ntraj ? g->ntraj : 1, sizeof(double));
     const size_t nt = g->ntraj ? g->ntraj : 1;
     g->hvvA = calloc(nt, sizeof *g->hvvA);
     g->hvvB = calloc(nt, sizeof *g->hvvB);
@@ -320,6 +338,7 @@ void orc_engine_destroy(OrcEngine* g) {
     if (!g) return;
     for (int k = 0; k < S_NSETS; ++k) free(g->set[k]);
     for (int k = 0; k < 3; ++k) free(g->cache[k]);
+    for (int k = 0; k < 3; ++k) free(g->dlj[k]);
     free(g->hvvA); free(g->hvvB); free(g->hvvC); free(g->rows_a); free(g->rows_b);
     free(g);
 }
@@ -342,6 +361,29 @@ void orc_set_state(OrcEngine* g, const double* mode1) {
 }
 void orc_get_state(const OrcEngine* g, double* mode1) {
     memcpy(mode1, g->set[S_PSI0], sizeof(double) * g->nbeam);
+}
+
+/* Plane / cylinder geometry of trajectory (t, q) at radius r (restatement,
+ * parity unpinned): weight w, direction factors n (1 - v.v' = 1 - n.n'
+ * after the constant term) and path cosine cdl. */
+static void geo34(const OrcEnv* v, int t, int q, double r, double* w, double* n, double* cdl) {
+    if (v->model == ORC_PLANE) {
+        const double ct = v->cos2[t], st = v->sin0[t];
+        *w = 1.0 / ((double)v->T * v->P);
+        n[0] = ct;
+        n[1] = st * v->cphi[q];
+        n[2] = st * v->sphi[q];
+        *cdl = ct;
+    } else {
+        const double ra = v->Rnu / r;
+        const double sa = ra * v->sin0[t];
+        const double ca = sqrt(1.0 - sa * sa);
+        *w = ra * (v->cos2[t] / ca) / ((double)v->T * v->P);
+        n[0] = v->cphi[q] * ca;
+        n[1] = v->cphi[q] * sa;
+        n[2] = v->sphi[q];
+        *cdl = n[0];
+    }
 }
 
 /* fill_cache, geometry.cpp:66-87 */
@@ -387,6 +429,27 @@ static void e_sum(const double* b, const double* fw, int E, double* row) {
 static void fold(const OrcEngine* g, const CacheRow* c, double (*rows)[3], double* out12) {
     const OrcEnv* v = g->env;
     for (int k = 0; k < 12; ++k) out12[k] = 0.0;
+    if (v->model >= ORC_PLANE) { /* per-trajectory weights, ascending trajectory order */
+        for (int jl = 0; jl < g->ntraj; ++jl) {
+            const int t = g->t_lo + jl / v->P, q = jl % v->P;
+            double R[3] = {0, 0, 0};
+            for (int s = 0; s < 4; ++s) {
+                const double* rw = rows[jl * 4 + s];
+                const double cs = v->coupling[s];
+                if (s & 1) { R[0] -= cs * rw[0]; R[1] -= cs * rw[1]; R[2] -= cs * (-rw[2]); }
+                else { R[0] += cs * rw[0]; R[1] += cs * rw[1]; R[2] += cs * rw[2]; }
+            }
+            double w, n[3], cdl;
+            geo34(v, t, q, c[0].w /* radius carried in w slot, see orc_prepare */, &w, n, &cdl);
+            for (int k = 0; k < 3; ++k) {
+                out12[k] += R[k] * w;
+                out12[3 + k] += R[k] * (w * n[0]);
+                out12[6 + k] += R[k] * (w * n[1]);
+                out12[9 + k] += R[k] * (w * n[2]);
+            }
+        }
+        return;
+    }
     for (int t = g->t_lo; t < g->t_hi; ++t) {
         double acc[3] = {0, 0, 0}, acc_c[3] = {0, 0, 0}, acc_s[3] = {0, 0, 0};
         for (int q = 0; q < v->P; ++q) {
@@ -439,6 +502,16 @@ static void fold(const OrcEngine* g, const CacheRow* c, double (*rows)[3], doubl
 static void assemble(const OrcEngine* g, const CacheRow* c, const double* s12, double r,
                      double (*dst)[3]) {
     const OrcEnv* v = g->env;
+    if (v->model >= ORC_PLANE) {
+        for (int jl = 0; jl < g->ntraj; ++jl) {
+            const int t = g->t_lo + jl / v->P, q = jl % v->P;
+            double w, n[3], cdl;
+            geo34(v, t, q, r, &w, n, &cdl);
+            for (int k = 0; k < 3; ++k)
+                dst[jl][k] = 0.5 * (s12[k] + s12[3 + k] * (-n[0]) + s12[6 + k] * (-n[1]) + s12[9 + k] * (-n[2]));
+        }
+        return;
+    }
     for (int t = g->t_lo; t < g->t_hi; ++t)
         for (int q = 0; q < v->P; ++q) {
             const int jl = (t - g->t_lo) * v->P + q;
@@ -470,7 +543,8 @@ static double pass(OrcEngine* g, double (*hvv)[3], int dl_slot, double A, int in
     double err = 0.0;
     for (int jl = 0; jl < g->ntraj; ++jl) {
         const int t = g->t_lo + jl / v->P;
-        const double dl = g->cache[dl_slot][t].dl;
+        const double dl = g->dlj[dl_slot][jl];
+        (void)t;
         for (int s = 0; s < 4; ++s) {
             double hb[3];
             if (s & 1) { hb[0] = -(hvv[jl][0] + 0.5 * A); hb[1] = -hvv[jl][1]; hb[2] = hvv[jl][2]; }
@@ -509,6 +583,27 @@ static void copy_set(OrcEngine* g, int dst, int src) {
 int orc_prepare(OrcEngine* g, double r, double dr) {
     g->r = r;
     g->dr = dr;
+    if (g->env->model >= ORC_PLANE) {
+        const OrcEnv* v = g->env;
+        const double rk[3] = {r, r + 0.5 * dr, r + dr};
+        if (v->model == ORC_CYLINDER && r < v->Rnu) {
+            set_err("cylinder: r below the emitting surface");
+            return 2;
+        }
+        for (int k = 0; k < 3; ++k) g->cache[k][0].w = rk[k]; /* radius for fold() */
+        for (int jl = 0; jl < g->ntraj; ++jl) {
+            const int t = g->t_lo + jl / v->P, q = jl % v->P;
+            double w, n[3], c[3];
+            for (int k = 0; k < 3; ++k) geo34(v, t, q, rk[k], &w, n, &c[k]);
+            g->dlj[0][jl] = 0.5 * dr / (0.5 * (c[0] + c[1]));
+            g->dlj[1][jl] = 0.5 * dr / (0.5 * (c[1] + c[2]));
+            g->dlj[2][jl] = dr / (0.5 * (c[0] + c[2]));
+        }
+        g->A[0] = orc_matter_potential(v, r);
+        g->A[1] = orc_matter_potential(v, r + 0.5 * dr);
+        g->A[2] = orc_matter_potential(v, r + dr);
+        return 0;
+    }
     if (g->env->model != ORC_SINGLE_ANGLE && r < g->env->Rnu) {
         set_err("fill_cache: r below the neutrino sphere");
         return 2;
@@ -525,6 +620,8 @@ int orc_prepare(OrcEngine* g, double r, double dr) {
         delta_ls(g, g->cache[1], g->cache[1], g->cache[2], 0.5 * dr);
         delta_ls(g, g->cache[2], g->cache[0], g->cache[2], dr);
     }
+    for (int jl = 0; jl < g->ntraj; ++jl)
+        for (int k = 0; k < 3; ++k) g->dlj[k][jl] = g->cache[k][g->t_lo + jl / g->env->P].dl;
     g->A[0] = orc_matter_potential(g->env, r);
     g->A[1] = orc_matter_potential(g->env, r + 0.5 * dr);
     g->A[2] = orc_matter_potential(g->env, r + dr);
@@ -668,5 +765,16 @@ int orc_run(OrcEngine* g, const OrcCtl* in, OrcSummary* out) {
     out->rejected = rej;
     out->final_max_norm_dev = orc_max_norm_dev(g);
     out->termination = term;
+    return 0;
+}
+
+/* fold_rows + combine_stage + assemble_hvv on caller-supplied rows
+ * ([local traj*4+s][3]) at radius r (test hook; mirrors ref_partial_hvv). */
+int orc_hvv_from_rows(OrcEngine* g, double r, const double* rows, double* sums12, double* hvv) {
+    int rc = orc_prepare(g, r, 0.0);
+    if (rc) return rc;
+    memcpy(g->rows_a, rows, sizeof(double) * 3 * 4 * (size_t)g->ntraj);
+    fold(g, g->cache[0], g->rows_a, sums12);
+    assemble(g, g->cache[0], sums12, r, (double(*)[3])hvv);
     return 0;
 }

@@ -20,7 +20,11 @@
 extern "C" {
 #endif
 
-enum { ORC_SINGLE_ANGLE = 0, ORC_BULB = 1, ORC_EXT_BULB = 2 };
+/* Models 0-2 restate the reference (geom::Model).  3 (plane, paper Eq. 3.19)
+ * and 4 (cylinder, Eq. 3.20) are BASELINE configs[3]/[4], which the reference
+ * does not implement: PARITY UNPINNED for those two (self-consistency tests
+ * only; see DESIGN.md §9 for the geometry chosen). */
+enum { ORC_SINGLE_ANGLE = 0, ORC_BULB = 1, ORC_EXT_BULB = 2, ORC_PLANE = 3, ORC_CYLINDER = 4 };
 enum { ORC_MATTER_POWERLAW = 0, ORC_MATTER_EXP = 1, ORC_MATTER_SUM = 2, ORC_MATTER_OFF = 3 };
 
 typedef struct {
@@ -90,6 +94,9 @@ typedef struct {
 int orc_run(OrcEngine* eng, const OrcCtl* ctl, OrcSummary* out);
 double orc_step_size_update(const OrcCtl* ctl, double err, int accepted, int* collapse);
 double orc_max_norm_dev(const OrcEngine* eng);
+
+/* fold_rows + combine_stage + assemble_hvv on given rows at radius r (tests). */
+int orc_hvv_from_rows(OrcEngine* eng, double r, const double* rows, double* sums12, double* hvv);
 
 /* make_partitions (parallel.cpp:11-24): out = [workers][2] (lo, hi). */
 int orc_make_partitions(int len, int workers, int* out);

@@ -223,6 +223,7 @@ def _olib():
         L.orc_max_norm_dev.argtypes = [C.c_void_p]
         L.orc_max_norm_dev.restype = C.c_double
         L.orc_make_partitions.argtypes = [C.c_int, C.c_int, C.POINTER(C.c_int)]
+        L.orc_hvv_from_rows.argtypes = [C.c_void_p, C.c_double, _dp, _dp, _dp]
         _oracle_lib = L
     return _oracle_lib
 
@@ -264,7 +265,7 @@ class Oracle:
         if p.model == 0:
             self.T, self.P = 1, 1
         else:
-            self.T, self.P = p.abins, (p.pbins if p.model == 2 else 1)
+            self.T, self.P = p.abins, (p.pbins if p.model >= 2 else 1)
         self.E = p.ebins
         self.t_lo = 0 if t_lo is None else t_lo
         self.t_hi = self.T if t_hi is None else t_hi
@@ -347,6 +348,13 @@ class Oracle:
         out = np.zeros(4)
         self.L.orc_evolve_bin(_ptr(h), dl, _ptr(psi), _ptr(out))
         return out
+
+    def hvv_from_rows(self, r, rows):
+        rows = np.ascontiguousarray(rows, dtype=np.float64)
+        ntraj = (self.t_hi - self.t_lo) * self.P
+        sums, hvv = np.zeros(12), np.zeros((ntraj, 3))
+        self._check(self.L.orc_hvv_from_rows(self.eng, r, _ptr(rows), _ptr(sums), _ptr(hvv)))
+        return sums, hvv
 
 
 def oracle_fermi_integral(k, eta):

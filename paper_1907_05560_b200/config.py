@@ -10,7 +10,8 @@ from __future__ import annotations
 
 from dataclasses import dataclass, field
 
-MODEL_IDS = {"sa": 0, "single-angle": 0, "bulb": 1, "ebulb": 2, "extended-bulb": 2}
+MODEL_IDS = {"sa": 0, "single-angle": 0, "bulb": 1, "ebulb": 2, "extended-bulb": 2,
+             "plane": 3, "cylinder": 4}  # plane/cylinder: BASELINE configs[3]/[4] (not in the reference)
 MATTER_IDS = {"powerlaw": 0, "exp": 1, "sum": 2}  # matter.hpp:9 (Off = 3)
 MATTER_OFF = 3
 
@@ -91,7 +92,7 @@ class RunConfig:
     def model_id(self) -> int:
         m = self.values["model"]
         if m not in MODEL_IDS:
-            raise ConfigError("model must be one of sa|bulb|ebulb, got: " + m)
+            raise ConfigError("model must be one of sa|bulb|ebulb|plane|cylinder, got: " + m)
         return MODEL_IDS[m]
 
     @property
@@ -140,7 +141,7 @@ class RunConfig:
             raise ConfigError("config: kappa must be in (0, 1]")
         if not v["eps0"] > 0.0:
             raise ConfigError("config: eps0 must be > 0")
-        if v["R0"] < v["Rv"]:
+        if v["R0"] < v["Rv"] and self.model_id != 3:
             raise ConfigError("config: R0 must be >= Rv")
         self.model_id
         self.matter_id
@@ -208,6 +209,14 @@ BASELINE_CONFIGS = {
     # configs[2]: large bulb, 4096 angle bins x 256 energy bins, 1000 steps
     "configs2": _COMMON + "model= bulb\nAbins= 4096\nPbins= 1\nEbins= 256\nhasMatter= 0\n"
     "perturb= 1e-10\nR0= 10\nRn= 250\ndr= 0.24\nmax_dr= 0.24\nTs= 1000\n",
+    # configs[3]: plane emission, 256 zenith x 64 azimuth x 64 energy bins, 1000
+    # fixed steps over 0-200 km, 1e-8 symmetry-breaking noise
+    "configs3": _COMMON + "model= plane\nAbins= 256\nPbins= 64\nEbins= 64\nhasMatter= 0\n"
+    "perturb= 1e-8\nR0= 0\nRn= 200\ndr= 0.2\nmax_dr= 0.2\nTs= 1000\n",
+    # configs[4]: line source (cylinder), 512 polar x 128 axial-tilt x 32 energy
+    # bins, 1000 fixed steps in distance from the axis 10-250 km
+    "configs4": _COMMON + "model= cylinder\nAbins= 512\nPbins= 128\nEbins= 32\nhasMatter= 0\n"
+    "perturb= 1e-8\nR0= 10\nRn= 250\ndr= 0.24\nmax_dr= 0.24\nTs= 1000\n",
 }
 
 

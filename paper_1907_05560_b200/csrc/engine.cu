@@ -99,7 +99,9 @@ StageFn stage_kernel(int model, int stage) {
     switch (model) {
         case 0: return stage_fn<0>(stage);
         case 1: return stage_fn<1>(stage);
-        default: return stage_fn<2>(stage);
+        case 2: return stage_fn<2>(stage);
+        case 3: return stage_fn<3>(stage);
+        default: return stage_fn<4>(stage);
     }
 }
 
@@ -249,7 +251,7 @@ struct OscCtx {
     }
 
     void check_radius(double r) const {
-        if (desc.model != OSC_MODEL_SINGLE_ANGLE && r < desc.Rnu)
+        if (desc.model != OSC_MODEL_SINGLE_ANGLE && desc.model != OSC_MODEL_PLANE && r < desc.Rnu)
             throw Error(OSC_ERR_NUMERIC, "fill_cache: r below the neutrino sphere");
         if (desc.matter_profile != OSC_MATTER_OFF && r < desc.Rnu)
             throw Error(OSC_ERR_NUMERIC, "baryon_density: r below the neutrino sphere");
@@ -308,7 +310,7 @@ __global__ void k_dfma_peak(double* out, int iters, double y, double z) {
 
 void validate(const OscDesc* d) {
     if (!d) throw Error(OSC_ERR_CONFIG, "osc_create: null desc");
-    if (d->model < 0 || d->model > 2) throw Error(OSC_ERR_CONFIG, "osc_create: bad model");
+    if (d->model < 0 || d->model > 4) throw Error(OSC_ERR_CONFIG, "osc_create: bad model");
     if (d->abins < 1 || d->pbins < 1 || d->ebins < 1)
         throw Error(OSC_ERR_CONFIG, "osc_create: Abins, Pbins, Ebins must be >= 1");
     if (d->model == OSC_MODEL_SINGLE_ANGLE && (d->abins != 1 || d->pbins != 1))
@@ -454,7 +456,11 @@ int osc_create(const OscDesc* desc, const OscComm* comm, OscCtx** out) {
         c->half2.alloc((size_t)c->npad * 16);
         a.Rnu = desc->Rnu;
         a.dcos2 = 1.0 / c->T;
-        a.phi_measure = desc->model == OSC_MODEL_EXT_BULB ? 1.0 / c->P : 1.0;
+        a.phi_measure = desc->model >= OSC_MODEL_EXT_BULB ? 1.0 / c->P : 1.0;
+        // plane: w = dcos / P;  cylinder: w = (R/rho)(cos a0/cos a) (da0 / pi) / P
+        a.wscale = desc->model == OSC_MODEL_PLANE ? 1.0 / ((double)c->T * c->P)
+                   : desc->model == OSC_MODEL_CYLINDER ? 1.0 / ((double)c->T * c->P)
+                                                        : 0.0;
         a.cos2 = c->cos2.p;
         a.sin0 = c->sin0.p;
         a.cphi = c->cphi.p;

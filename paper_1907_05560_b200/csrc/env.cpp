@@ -122,16 +122,34 @@ int osc_env_build(const OscParams* p, OscEnv** out) {
             throw Error(OSC_ERR_CONFIG, "build_spectrum: need E1 > E0 >= 0");
         env->cos2.resize(T);
         env->sin0.resize(T);
-        for (int t = 0; t < T; ++t) {
-            env->cos2[t] = (t + 0.5) / T;
-            env->sin0[t] = std::sqrt(1.0 - env->cos2[t]);
-        }
         env->cphi.resize(P);
         env->sphi.resize(P);
-        const double dphi = 2.0 * oscb200::kPi / P;
-        for (int q = 0; q < P; ++q) {
-            env->cphi[q] = std::cos((q + 0.5) * dphi);
-            env->sphi[q] = std::sin((q + 0.5) * dphi);
+        if (p->model == OSC_MODEL_CYLINDER) {
+            // in-plane emission angle a0: midpoints uniform on (-pi/2, pi/2);
+            // axial tilt b: midpoints uniform in sin(b) on (-1, 1)
+            for (int t = 0; t < T; ++t) {
+                const double a0 = -0.5 * oscb200::kPi + (t + 0.5) * oscb200::kPi / T;
+                env->cos2[t] = std::cos(a0);
+                env->sin0[t] = std::sin(a0);
+            }
+            for (int q = 0; q < P; ++q) {
+                const double sb = -1.0 + (q + 0.5) * 2.0 / P;
+                env->sphi[q] = sb;
+                env->cphi[q] = std::sqrt(1.0 - sb * sb);
+            }
+        } else {
+            for (int t = 0; t < T; ++t) {
+                // bulb: midpoints in cos^2(theta0) (geometry.cpp:52-55);
+                // plane: midpoints in cos(theta) on (0, 1]
+                const double u = (t + 0.5) / T;
+                env->cos2[t] = u;
+                env->sin0[t] = p->model == OSC_MODEL_PLANE ? std::sqrt(1.0 - u * u) : std::sqrt(1.0 - u);
+            }
+            const double dphi = 2.0 * oscb200::kPi / P;
+            for (int q = 0; q < P; ++q) {
+                env->cphi[q] = std::cos((q + 0.5) * dphi);
+                env->sphi[q] = std::sin((q + 0.5) * dphi);
+            }
         }
         const double dE = (p->E1 - p->E0) / E;
         const double c2 = std::cos(2.0 * p->theta), s2 = std::sin(2.0 * p->theta);
