@@ -75,6 +75,14 @@ typedef struct OscDesc {
     double perturb;            /* Environment::perturb                        */
     int matter_profile;        /* OSC_MATTER_*  (MatterParams, matter.hpp:11) */
     double Ye, nb0, hNS, Mns, gs, S;
+    /* 3-flavour extension (BASELINE configs[1]; not in the reference).
+     * nflav 0 or 2: the fields above; nflav 3: species nu_e, nubar_e, nu_mu,
+     * nubar_mu, nu_tau, nubar_tau, state comps re/im of (e, mu, tau), and the
+     * tables below replace vac_h11/vac_h12/fw/couplings.  Models 0-1 only. */
+    int nflav;
+    const double* vac3;        /* [ebins][9] H_vac: d_e d_mu d_tau, re/im h_emu h_etau h_mutau */
+    const double* fw6;         /* [6][ebins] f*dE per species */
+    double couplings6[6];
 } OscDesc;
 
 /* One process per GPU.  nranks == 1 -> no collectives.  For nranks > 1 all
@@ -186,6 +194,12 @@ typedef struct OscParams {
     double L[4], T[4], Emean[4], eta[4];
     int matter_profile;
     double Ye, nb0, hNS, Mns, gs, S;
+    /* nflav = 3: dm2 / theta above are dm2_21 / theta12; the tau species take
+     * L_tau / T_tau / Emean_tau / eta_tau (index 0 nu_tau, 1 nubar_tau); the
+     * mu species take the x entries (index 2, 3) of the arrays above. */
+    int nflav;
+    double dm2_31, theta13, theta23, delta_cp;
+    double L_tau[2], T_tau[2], Emean_tau[2], eta_tau[2];
 } OscParams;
 typedef struct OscEnv OscEnv;
 int osc_env_build(const OscParams* p, OscEnv** out);

@@ -101,6 +101,36 @@ int orc_hvv_from_rows(OrcEngine* eng, double r, const double* rows, double* sums
 /* make_partitions (parallel.cpp:11-24): out = [workers][2] (lo, hi). */
 int orc_make_partitions(int len, int workers, int* out);
 
+/* ---- 3-flavour restatement (oscflat3_oracle.c; BASELINE configs[1];
+ * PARITY UNPINNED w.r.t. the reference, which supports Flvs = 2 only). */
+typedef struct {
+    int model, abins, pbins, ebins;
+    double Rnu, E0, E1, dm21, dm31, th12, th13, th23, dcp, hvv_scale, perturb;
+    double L[6], T[6], Emean[6], eta[6];
+    int matter_profile;
+    double Ye, nb0, hNS, Mns, gs, S;
+} Orc3Params;
+
+typedef struct Orc3Env Orc3Env;
+typedef struct Orc3Engine Orc3Engine;
+const char* orc3_last_error(void);
+int orc3_env_create(const Orc3Params* p, Orc3Env** out);
+void orc3_env_destroy(Orc3Env* env);
+void orc3_env_tables(const Orc3Env* env, double* vac9E, double* fw6E, double* couplings6);
+void orc3_expm(const double* h9, double tau, double* out18);
+void orc3_init_state(int species, int ebins, double eps, uint64_t seed, double* out6E);
+int orc3_engine_create(const Orc3Env* env, int t_lo, int t_hi, Orc3Engine** out);
+void orc3_engine_destroy(Orc3Engine* eng);
+void orc3_init_states(Orc3Engine* eng);
+void orc3_set_state(Orc3Engine* eng, const double* mode1);
+void orc3_get_state(const Orc3Engine* eng, double* mode1);
+int orc3_prepare(Orc3Engine* eng, double r, double dr);
+int orc3_stage(Orc3Engine* eng, int stage, double* partial);
+int orc3_stage_set(Orc3Engine* eng, int stage, const double* total);
+void orc3_commit(Orc3Engine* eng);
+int orc3_trial_step(Orc3Engine* eng, double r, double dr, double* err);
+int orc3_run(Orc3Engine* eng, const OrcCtl* ctl, OrcSummary* out);
+
 #ifdef __cplusplus
 }
 #endif

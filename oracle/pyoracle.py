@@ -243,6 +243,122 @@ def params_from_config(cfg) -> _Params:
     return p
 
 
+class _Params3(C.Structure):
+    _fields_ = [("model", C.c_int), ("abins", C.c_int), ("pbins", C.c_int), ("ebins", C.c_int),
+                ("Rnu", C.c_double), ("E0", C.c_double), ("E1", C.c_double),
+                ("dm21", C.c_double), ("dm31", C.c_double), ("th12", C.c_double),
+                ("th13", C.c_double), ("th23", C.c_double), ("dcp", C.c_double),
+                ("hvv_scale", C.c_double), ("perturb", C.c_double), ("L", C.c_double * 6),
+                ("T", C.c_double * 6), ("Emean", C.c_double * 6), ("eta", C.c_double * 6),
+                ("matter_profile", C.c_int), ("Ye", C.c_double), ("nb0", C.c_double),
+                ("hNS", C.c_double), ("Mns", C.c_double), ("gs", C.c_double), ("S", C.c_double)]
+
+
+def params3_from_config(cfg) -> _Params3:
+    v, prov = cfg.values, cfg.provided
+    p = _Params3()
+    p.model = cfg.model_id
+    p.abins, p.pbins, p.ebins = v["Abins"], v["Pbins"], v["Ebins"]
+    p.Rnu, p.E0, p.E1 = v["Rv"], v["E0"], v["E1"]
+    p.dm21 = v["dm2_21"] if "dm2_21" in prov else v["dm2"]
+    p.th12 = v["theta12"] if "theta12" in prov else v["theta"]
+    p.dm31, p.th13, p.th23, p.dcp = v["dm2_31"], v["theta13"], v["theta23"], v["deltaCP"]
+    p.hvv_scale, p.perturb = v["hvvScale"], v["perturb"]
+    for arr, name in ((p.L, "L"), (p.T, "T"), (p.Emean, "E"), (p.eta, "eta")):
+        vals = cfg.species(name) + cfg.tau(name)
+        for i, x in enumerate(vals):
+            arr[i] = x
+    p.matter_profile = cfg.matter_id
+    p.Ye, p.nb0, p.hNS, p.Mns, p.gs, p.S = v["Ye"], v["nb0"], v["hNS"], v["Mns"], v["gs"], v["S"]
+    return p
+
+
+class Oracle3:
+    """3-flavour C restatement (oracle/oscflat3_oracle.c; parity unpinned)."""
+
+    def __init__(self, cfg, t_lo=None, t_hi=None):
+        self.L = L = _olib()
+        for f in ("orc3_env_create", "orc3_engine_create"):
+            pass
+        L.orc3_last_error.restype = C.c_char_p
+        L.orc3_env_create.argtypes = [C.POINTER(_Params3), C.POINTER(C.c_void_p)]
+        L.orc3_env_destroy.argtypes = [C.c_void_p]
+        L.orc3_env_tables.argtypes = [C.c_void_p, _dp, _dp, _dp]
+        L.orc3_engine_create.argtypes = [C.c_void_p, C.c_int, C.c_int, C.POINTER(C.c_void_p)]
+        L.orc3_engine_destroy.argtypes = [C.c_void_p]
+        L.orc3_init_states.argtypes = [C.c_void_p]
+        L.orc3_set_state.argtypes = [C.c_void_p, _dp]
+        L.orc3_get_state.argtypes = [C.c_void_p, _dp]
+        L.orc3_trial_step.argtypes = [C.c_void_p, C.c_double, C.c_double, _dp]
+        L.orc3_run.argtypes = [C.c_void_p, C.POINTER(_Ctl), C.POINTER(_Summary)]
+        L.orc3_expm.argtypes = [_dp, C.c_double, _dp]
+        self.cfg = cfg
+        self.params = params3_from_config(cfg)
+        env = C.c_void_p()
+        if L.orc3_env_create(C.byref(self.params), C.byref(env)) != 0:
+            raise RuntimeError(L.orc3_last_error().decode())
+        self.env = env
+        p = self.params
+        self.T = 1 if p.model == 0 else p.abins
+        self.P = 1
+        self.E = p.ebins
+        self.t_lo = 0 if t_lo is None else t_lo
+        self.t_hi = self.T if t_hi is None else t_hi
+        eng = C.c_void_p()
+        if L.orc3_engine_create(env, self.t_lo, self.t_hi, C.byref(eng)) != 0:
+            raise RuntimeError(L.orc3_last_error().decode())
+        self.eng = eng
+        self.n = (self.t_hi - self.t_lo) * self.P * 36 * self.E
+        L.orc3_init_states(eng)
+
+    def __del__(self):
+        try:
+            self.L.orc3_engine_destroy(self.eng)
+            self.L.orc3_env_destroy(self.env)
+        except Exception:
+            pass
+
+    def _check(self, rc):
+        if rc != 0:
+            raise RuntimeError(f"oracle3 error {rc}: {self.L.orc3_last_error().decode()}")
+
+    def tables(self):
+        E = self.E
+        vac, fw, c = np.zeros(9 * E), np.zeros(6 * E), np.zeros(6)
+        self.L.orc3_env_tables(self.env, _ptr(vac), _ptr(fw), _ptr(c))
+        return dict(vac3=vac.reshape(E, 9), fw6=fw.reshape(6, E), couplings6=c)
+
+    def get_state(self):
+        out = np.zeros(self.n)
+        self.L.orc3_get_state(self.eng, _ptr(out))
+        return out
+
+    def set_state(self, mode1):
+        a = np.ascontiguousarray(mode1, dtype=np.float64).ravel()
+        self.L.orc3_set_state(self.eng, _ptr(a))
+
+    def trial_step(self, r, dr):
+        err = C.c_double()
+        self._check(self.L.orc3_trial_step(self.eng, r, dr, C.byref(err)))
+        return err.value
+
+    def run(self, r=None, dr=None, it=0, ts=None):
+        v = self.cfg.values
+        c = _Ctl(dr=v["dr"] if dr is None else dr, dr_max=v["max_dr"], dr_min=v["min_dr"],
+                 eps0=v["eps0"], kappa=v["kappa"], r=v["R0"] if r is None else r, R0=v["R0"],
+                 Rn=v["Rn"], iter=it, Ts=v["Ts"] if ts is None else ts)
+        s = _Summary()
+        self._check(self.L.orc3_run(self.eng, C.byref(c), C.byref(s)))
+        return dict(final_r=s.final_r, iterations=s.iterations, accepted=s.accepted,
+                    rejected=s.rejected, final_max_norm_dev=s.final_max_norm_dev)
+
+    def expm(self, h9, tau):
+        h9 = np.ascontiguousarray(h9, dtype=np.float64)
+        out = np.zeros(18)
+        self.L.orc3_expm(_ptr(h9), tau, _ptr(out))
+        return out[0::2].reshape(3, 3) + 1j * out[1::2].reshape(3, 3)
+
+
 def make_partitions(length: int, workers: int):
     out = (C.c_int * (2 * workers))()
     if _olib().orc_make_partitions(length, workers, out) != 0:

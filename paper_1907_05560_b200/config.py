@@ -20,6 +20,9 @@ _FLOAT = {
     "hvvScale", "perturb", "Ye", "nb0", "Rv", "Mns", "gs", "S", "hNS",
     "Lve", "Lvae", "Lvt", "Lvat", "Tve", "Tvae", "Tvt", "Tvat", "Eve", "Evae", "Evt", "Evat",
     "eta_ve", "eta_vae", "eta_vt", "eta_vat",
+    # 3-flavour extension (BASELINE configs[1]; the reference accepts Flvs = 2 only)
+    "dm2_21", "dm2_31", "theta12", "theta13", "theta23", "deltaCP",
+    "Lvtau", "Lvatau", "Tvtau", "Tvatau", "Evtau", "Evatau", "eta_vtau", "eta_vatau",
 }
 _INT = {"Ts", "Abins", "Pbins", "Ebins", "SPoints", "Flvs", "lanes", "hasMatter"}
 _STR = {"model", "matterProfile"}
@@ -104,6 +107,14 @@ class RunConfig:
             raise ConfigError("matterProfile must be powerlaw|exp|sum, got: " + p)
         return MATTER_IDS[p]
 
+    def tau(self, name: str) -> list:
+        """3-flavour tau-sector spectrum keys; default to the x species."""
+        keys = {"L": (("Lvtau", "Lvt"), ("Lvatau", "Lvat")),
+                "T": (("Tvtau", "Tvt"), ("Tvatau", "Tvat")),
+                "E": (("Evtau", "Evt"), ("Evatau", "Evat")),
+                "eta": (("eta_vtau", "eta_vt"), ("eta_vatau", "eta_vat"))}[name]
+        return [self.values[k] if k in self.provided else self.values[d] for k, d in keys]
+
     def species(self, name: str) -> list:
         keys = {"L": ("Lve", "Lvae", "Lvt", "Lvat"), "T": ("Tve", "Tvae", "Tvt", "Tvat"),
                 "E": ("Eve", "Evae", "Evt", "Evat"),
@@ -135,8 +146,10 @@ class RunConfig:
             raise ConfigError("config: need E0 < E1")
         if min(v["Abins"], v["Pbins"], v["Ebins"]) < 1:
             raise ConfigError("config: Abins, Pbins, Ebins must be >= 1")
-        if v["Flvs"] != 2:
-            raise ConfigError("config: only Flvs= 2 is supported")
+        if v["Flvs"] not in (2, 3):
+            raise ConfigError("config: Flvs must be 2 or 3")
+        if v["Flvs"] == 3 and self.model_id > 1:
+            raise ConfigError("config: Flvs= 3 supports the sa and bulb models")
         if not (0.0 < v["kappa"] <= 1.0):
             raise ConfigError("config: kappa must be in (0, 1]")
         if not v["eps0"] > 0.0:
@@ -209,6 +222,14 @@ BASELINE_CONFIGS = {
     # configs[2]: large bulb, 4096 angle bins x 256 energy bins, 1000 steps
     "configs2": _COMMON + "model= bulb\nAbins= 4096\nPbins= 1\nEbins= 256\nhasMatter= 0\n"
     "perturb= 1e-10\nR0= 10\nRn= 250\ndr= 0.24\nmax_dr= 0.24\nTs= 1000\n",
+    # configs[1]: 3-flavour bulb, 512 angle x 128 energy bins, power-law matter
+    # normalised to Ye = 0.5, rho = 1e7 g/cm^3 at 100 km (gs scales the
+    # reference's 4.2e30 (10 km/r)^3 law: n_b(100 km) = 1e7 / m_u), 4000 fixed
+    # steps over 10-250 km (range not given by BASELINE)
+    "configs1": _COMMON + "Flvs= 3\nmodel= bulb\nAbins= 512\nPbins= 1\nEbins= 128\n"
+    "dm2_21= 7.5e-5\ndm2_31= -2.4e-3\ntheta12= 0.59\ntheta13= 0.15\ntheta23= 0.785\n"
+    "deltaCP= 0\nhasMatter= 1\nmatterProfile= powerlaw\nYe= 0.5\nMns= 1.4\nS= 100\n"
+    "gs= 1433.8282\nperturb= 1e-10\nR0= 10\nRn= 250\ndr= 0.06\nmax_dr= 0.06\nTs= 4000\n",
     # configs[3]: plane emission, 256 zenith x 64 azimuth x 64 energy bins, 1000
     # fixed steps over 0-200 km, 1e-8 symmetry-breaking noise
     "configs3": _COMMON + "model= plane\nAbins= 256\nPbins= 64\nEbins= 64\nhasMatter= 0\n"

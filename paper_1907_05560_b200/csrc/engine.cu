@@ -18,6 +18,7 @@
 
 #include "oscflat_b200.h"
 #include "status.hpp"
+#include "step3_kernels.cuh"
 #include "step_kernels.cuh"
 
 namespace oscb200 {
@@ -95,7 +96,17 @@ StageFn stage_fn(int stage) {
         default: return k_stage<MODEL, 4>;
     }
 }
-StageFn stage_kernel(int model, int stage) {
+template <int MODEL>
+StageFn stage3_fn(int stage) {
+    switch (stage) {
+        case 0: return k_stage3<MODEL, 0>;
+        case 2: return k_stage3<MODEL, 2>;
+        case 3: return k_stage3<MODEL, 3>;
+        default: return k_stage3<MODEL, 4>;
+    }
+}
+StageFn stage_kernel(int nflav, int model, int stage) {
+    if (nflav == 3) return model == 0 ? stage3_fn<0>(stage) : stage3_fn<1>(stage);
     switch (model) {
         case 0: return stage_fn<0>(stage);
         case 1: return stage_fn<1>(stage);
@@ -135,6 +146,9 @@ struct OscCtx {
     int nsm = 0, nblocks = 0, chunk = 0, ntr_max = 0;
     uint32_t e_magic = 0, e_shift = 0;
     int schedule = 1;  // 1: stash half2 (default), 0: recompute it in S4
+    int nflav = 2;
+    int nplanes = 16;  // state planes per buffer
+    DevBuf<double> vac3;
     int use_pdl = 1;
     cudaStream_t stream = nullptr;
     nccl::Comm comm = nullptr;
@@ -165,11 +179,11 @@ struct OscCtx {
     // one is scheduled while its predecessor drains (griddepcontrol in the
     // kernels orders the dependent reads).
     void launch_stage(int stage) {
-        const StageFn fn = stage_kernel(desc.model, stage);
+        const StageFn fn = stage_kernel(nflav, desc.model, stage);
         cudaLaunchConfig_t cfg{};
         cfg.gridDim = dim3(nblocks);
         cfg.blockDim = dim3(kBlock);
-        cfg.dynamicSmemBytes = stage_smem_bytes(stage, schedule, ntr_max);
+        cfg.dynamicSmemBytes = nflav == 3 ? stage3_smem_bytes(ntr_max) : stage_smem_bytes(stage, schedule, ntr_max);
         cfg.stream = stream;
         cudaLaunchAttribute attr[1];
         attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -317,6 +331,10 @@ void validate(const OscDesc* d) {
         throw Error(OSC_ERR_CONFIG, "single-angle model needs abins = pbins = 1");
     if (d->model == OSC_MODEL_BULB && d->pbins != 1)
         throw Error(OSC_ERR_CONFIG, "bulb model needs pbins = 1");
+    if (d->nflav != 0 && d->nflav != 2 && d->nflav != 3)
+        throw Error(OSC_ERR_CONFIG, "osc_create: only 2 or 3 flavours are supported");
+    if (d->nflav == 3 && (d->model > OSC_MODEL_BULB || !d->vac3 || !d->fw6))
+        throw Error(OSC_ERR_CONFIG, "3 flavours: single-angle / bulb models with vac3 and fw6 tables");
     if (!d->cos2_theta0 || !d->sin_theta0 || !d->cos_phi || !d->sin_phi || !d->vac_h11 ||
         !d->vac_h12 || !d->fw)
         throw Error(OSC_ERR_CONFIG, "osc_create: null table");
@@ -383,12 +401,18 @@ int osc_create(const OscDesc* desc, const OscComm* comm, OscCtx** out) {
         upload(c->sphi, desc->sin_phi, c->P);
         upload(c->vac11, desc->vac_h11, c->E);
         upload(c->vac12, desc->vac_h12, c->E);
-        std::vector<double> g(4 * static_cast<size_t>(c->E));
-        for (int s = 0; s < 4; ++s)
+        c->nflav = desc->nflav == 3 ? 3 : 2;
+        c->nplanes = c->nflav == 3 ? 36 : 16;
+        const int nsp = c->nflav == 3 ? 6 : 4;
+        const double* fw = c->nflav == 3 ? desc->fw6 : desc->fw;
+        const double* cpl = c->nflav == 3 ? desc->couplings6 : desc->couplings;
+        std::vector<double> g(nsp * static_cast<size_t>(c->E));
+        for (int s = 0; s < nsp; ++s)
             for (int e = 0; e < c->E; ++e)
-                g[(size_t)s * c->E + e] = ((s & 1) ? -1.0 : 1.0) * desc->couplings[s] * desc->fw[(size_t)s * c->E + e];
+                g[(size_t)s * c->E + e] = ((s & 1) ? -1.0 : 1.0) * cpl[s] * fw[(size_t)s * c->E + e];
         upload(c->g, g.data(), g.size());
-        const size_t plane = (size_t)c->npad * 16;
+        if (c->nflav == 3) upload(c->vac3, desc->vac3, 9 * (size_t)c->E);
+        const size_t plane = (size_t)c->npad * c->nplanes;
         c->psi[0].alloc(plane);
         c->psi[1].alloc(plane);
         CUDA_OK(cudaMemset(c->psi[0].p, 0, plane * sizeof(double)));
@@ -411,16 +435,19 @@ int osc_create(const OscDesc* desc, const OscComm* comm, OscCtx** out) {
         {
             const int occ = OSC_MIN_BLOCKS;
             const int nb = std::max(1, c->nsm * occ);
-            int chunk = (c->ncell + nb - 1) / nb;
+            // 3 flavours: blocks split in halves by particle class
+            const int per = c->nflav == 3 ? nb / 2 : nb;
+            int chunk = (c->ncell + per - 1) / per;
             chunk = std::max(32, (chunk + 31) / 32 * 32);
-            c->nblocks = nb;
+            c->nblocks = c->nflav == 3 ? 2 * per : nb;
             c->chunk = chunk;
             c->ntr_max = chunk / c->E + 2;
-            const size_t smax = stage_smem_bytes(4, 1, c->ntr_max);
+            const size_t smax =
+                c->nflav == 3 ? stage3_smem_bytes(c->ntr_max) : stage_smem_bytes(4, 1, c->ntr_max);
             if (smax > 200 * 1024)
                 throw Error(OSC_ERR_CONFIG, "osc_create: trajectory records exceed shared memory");
             for (int st : {0, 2, 3, 4})
-                CUDA_OK(cudaFuncSetAttribute(stage_kernel(desc->model, st),
+                CUDA_OK(cudaFuncSetAttribute(stage_kernel(c->nflav, desc->model, st),
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smax));
             // magic numbers for the division by E inside the kernels
             uint32_t l = 0;
@@ -453,7 +480,7 @@ int osc_create(const OscDesc* desc, const OscComm* comm, OscCtx** out) {
         a.e_magic = c->e_magic;
         a.e_shift = c->e_shift;
         a.schedule = c->schedule;
-        c->half2.alloc((size_t)c->npad * 16);
+        c->half2.alloc((size_t)c->npad * c->nplanes);
         a.Rnu = desc->Rnu;
         a.dcos2 = 1.0 / c->T;
         a.phi_measure = desc->model >= OSC_MODEL_EXT_BULB ? 1.0 / c->P : 1.0;
@@ -468,6 +495,9 @@ int osc_create(const OscDesc* desc, const OscComm* comm, OscCtx** out) {
         a.vac11 = c->vac11.p;
         a.vac12 = c->vac12.p;
         a.g = c->g.p;
+        a.vac3 = c->vac3.p;
+        a.nmom = c->nflav == 3 ? 36 : 12;
+        a.nplanes = c->nplanes;
         a.matter_profile = desc->matter_profile;
         a.Ye = desc->Ye;
         a.nb0 = desc->nb0;
@@ -501,21 +531,24 @@ int osc_local_range(const OscCtx* c, int* t_lo, int* t_hi, size_t* n) {
         if (!c) throw Error(OSC_ERR_CONFIG, "null context");
         if (t_lo) *t_lo = c->t_lo;
         if (t_hi) *t_hi = c->t_hi;
-        if (n) *n = (size_t)c->ncell * 16;
+        if (n) *n = (size_t)c->ncell * c->nplanes;
     });
 }
 
 int osc_init_states(OscCtx* c) {
     return guarded([&] {
         CUDA_OK(cudaSetDevice(c->device));
-        k_init<<<(c->ncell + 255) / 256, 256, 0, c->stream>>>(c->args, c->desc.perturb);
+        if (c->nflav == 3)
+            k_init3<<<(c->ncell + 255) / 256, 256, 0, c->stream>>>(c->args, c->desc.perturb);
+        else
+            k_init<<<(c->ncell + 255) / 256, 256, 0, c->stream>>>(c->args, c->desc.perturb);
         CUDA_OK(cudaGetLastError());
         CUDA_OK(cudaStreamSynchronize(c->stream));
     });
 }
 
 static void set_state_impl(OscCtx* c, const double* src, size_t n, cudaMemcpyKind kind) {
-    const size_t want = (size_t)c->ncell * 16;
+    const size_t want = (size_t)c->ncell * c->nplanes;
     if (n != want) throw Error(OSC_ERR_IO, "fill_mode1: payload size does not match the configured problem");
     CUDA_OK(cudaSetDevice(c->device));
     if (c->staging.n < want) c->staging.alloc(want);
@@ -526,7 +559,7 @@ static void set_state_impl(OscCtx* c, const double* src, size_t n, cudaMemcpyKin
 }
 
 static void get_state_impl(OscCtx* c, double* dst, size_t n, cudaMemcpyKind kind) {
-    const size_t want = (size_t)c->ncell * 16;
+    const size_t want = (size_t)c->ncell * c->nplanes;
     if (n != want) throw Error(OSC_ERR_IO, "extract_mode1: payload size mismatch");
     CUDA_OK(cudaSetDevice(c->device));
     if (c->staging.n < want) c->staging.alloc(want);
@@ -637,7 +670,7 @@ int osc_set_schedule(OscCtx* c, int schedule) {
     return guarded([&] {
         CUDA_OK(cudaSetDevice(c->device));
         if (schedule != 0 && schedule != 1) throw Error(OSC_ERR_CONFIG, "schedule must be 0 or 1");
-        if (schedule == 1 && !c->half2.p) c->half2.alloc((size_t)c->npad * 16);
+        if (schedule == 1 && !c->half2.p) c->half2.alloc((size_t)c->npad * c->nplanes);
         c->schedule = schedule;
         c->args.schedule = schedule;
         c->args.half2 = c->half2.p;
@@ -752,7 +785,7 @@ int osc_run(OscCtx* c, const OscStepControl* ctl, osc_hook_fn hook, void* user, 
             if (hook && c->h_ctl->accepted != last_acc) {
                 last_acc = c->h_ctl->accepted;
                 const auto ti = Clock::now();
-                host_state.resize((size_t)c->ncell * 16);
+                host_state.resize((size_t)c->ncell * c->nplanes);
                 get_state_impl(c, host_state.data(), host_state.size(), cudaMemcpyDeviceToHost);
                 OscHookInfo info{c->h_ctl->iter, c->h_ctl->r, c->h_ctl->dr, secs()};
                 hook(user, &info, host_state.data(), host_state.size());

@@ -7,7 +7,9 @@
 //   spectra        SpectrumTable ctor       spectra.cpp:87-125
 //   Fermi integral fermi_integral           spectra.cpp:17-83
 //   couplings      hvv_coupling_per_km      units.hpp:55-61
+#include <algorithm>
 #include <cmath>
+#include <complex>
 #include <cstring>
 #include <new>
 #include <stdexcept>
@@ -95,6 +97,8 @@ double coupling_per_km(double L, double Em, double Rnu) {
 struct OscEnv {
     OscDesc desc{};
     std::vector<double> cos2, sin0, cphi, sphi, vac11, vac12, fw;
+    std::vector<double> vac3, fw6;  // 3-flavour tables
+    double cpl6[6]{};
     double emean[4]{};
 };
 
@@ -161,30 +165,74 @@ int osc_env_build(const OscParams* p, OscEnv** out) {
             env->vac11[e] = -0.5 * delta * c2;
             env->vac12[e] = 0.5 * delta * s2;
         }
-        env->fw.resize(4 * static_cast<size_t>(E));
-        double cpl[4];
-        for (int s = 0; s < 4; ++s) {
-            const double eta = p->eta[s];
+        // SpectrumTable (spectra.cpp:87-125) + coupling (solver.cpp:71-85)
+        auto spectrum = [&](double L, double Tin, double Emean, double eta, double* row, double* em) {
             double T_s, Em;
-            if (p->T[s] > 0.0) {
-                T_s = p->T[s];
+            if (Tin > 0.0) {
+                T_s = Tin;
                 Em = oscb200::mean_energy(T_s, eta);
-            } else if (p->Emean[s] > 0.0) {
-                Em = p->Emean[s];
+            } else if (Emean > 0.0) {
+                Em = Emean;
                 T_s = Em * oscb200::fermi_integral(2, eta) / oscb200::fermi_integral(3, eta);
             } else {
                 throw Error(OSC_ERR_CONFIG, "build_spectrum: one of T or Emean must be positive");
             }
             // the coupling takes the configured mean energy when given
-            const double Em_c = p->Emean[s] > 0.0 ? p->Emean[s] : oscb200::mean_energy(p->T[s], eta);
-            cpl[s] = p->hvv_scale * oscb200::coupling_per_km(p->L[s], Em_c, p->Rnu);
-            env->emean[s] = Em;
+            const double Em_c = Emean > 0.0 ? Emean : oscb200::mean_energy(Tin, eta);
+            *em = Em;
             const double norm = 1.0 / (oscb200::fermi_integral(2, eta) * T_s * T_s * T_s);
             for (int e = 0; e < E; ++e) {
                 const double Ec = p->E0 + (e + 0.5) * dE;
                 const double x = Ec / T_s - eta;
                 const double den = x > 500.0 ? std::exp(x) : std::exp(x) + 1.0;
-                env->fw[static_cast<size_t>(s) * E + e] = norm * Ec * Ec / den * dE;
+                row[e] = norm * Ec * Ec / den * dE;
+            }
+            return p->hvv_scale * oscb200::coupling_per_km(L, Em_c, p->Rnu);
+        };
+        env->fw.resize(4 * static_cast<size_t>(E));
+        double cpl[4];
+        for (int s = 0; s < 4; ++s)
+            cpl[s] = spectrum(p->L[s], p->T[s], p->Emean[s], p->eta[s], env->fw.data() + (size_t)s * E,
+                              &env->emean[s]);
+        const bool three = p->nflav == 3;
+        if (three) {
+            if (p->model > OSC_MODEL_BULB)
+                throw Error(OSC_ERR_CONFIG, "3 flavours: single-angle and bulb models only");
+            // species nu_e, nubar_e, nu_mu, nubar_mu (= the x spectra), nu_tau, nubar_tau
+            env->fw6.resize(6 * static_cast<size_t>(E));
+            std::copy(env->fw.begin(), env->fw.end(), env->fw6.begin());
+            for (int s = 0; s < 4; ++s) env->cpl6[s] = cpl[s];
+            double em;
+            for (int k = 0; k < 2; ++k)
+                env->cpl6[4 + k] = spectrum(p->L_tau[k], p->T_tau[k], p->Emean_tau[k], p->eta_tau[k],
+                                            env->fw6.data() + (size_t)(4 + k) * E, &em);
+            // H_vac = U diag(0, dm21, dm31) U^dagger / 2E, standard PMNS
+            // parametrisation (theta12 = theta, dm21 = dm2)
+            using cd = std::complex<double>;
+            const double c12 = std::cos(p->theta), s12 = std::sin(p->theta);
+            const double c13 = std::cos(p->theta13), s13 = std::sin(p->theta13);
+            const double c23 = std::cos(p->theta23), s23 = std::sin(p->theta23);
+            const cd ed = std::exp(cd(0.0, p->delta_cp));
+            const cd U[3][3] = {{c12 * c13, s12 * c13, s13 * std::conj(ed)},
+                                {-s12 * c23 - c12 * s23 * s13 * ed, c12 * c23 - s12 * s23 * s13 * ed, s23 * c13},
+                                {s12 * s23 - c12 * c23 * s13 * ed, -c12 * s23 - s12 * c23 * s13 * ed, c23 * c13}};
+            env->vac3.resize(9 * static_cast<size_t>(E));
+            for (int e = 0; e < E; ++e) {
+                const double Ec = p->E0 + (e + 0.5) * dE;
+                const double lam[3] = {0.0, (p->dm2 * 1e-12 / (2.0 * Ec)) / oscb200::kHcKm,
+                                       (p->dm2_31 * 1e-12 / (2.0 * Ec)) / oscb200::kHcKm};
+                cd H[3][3];
+                for (int i = 0; i < 3; ++i)
+                    for (int j = 0; j < 3; ++j) {
+                        cd acc = 0.0;
+                        for (int k = 0; k < 3; ++k) acc += U[i][k] * lam[k] * std::conj(U[j][k]);
+                        H[i][j] = acc;
+                    }
+                double* o = env->vac3.data() + 9 * (size_t)e;
+                o[0] = H[0][0].real(); o[1] = H[1][1].real(); o[2] = H[2][2].real();
+                o[3] = H[0][1].real(); o[4] = H[0][1].imag();
+                o[5] = H[0][2].real(); o[6] = H[0][2].imag();
+                o[7] = H[1][2].real(); o[8] = H[1][2].imag();
             }
         }
         OscDesc& d = env->desc;
@@ -209,6 +257,12 @@ int osc_env_build(const OscParams* p, OscEnv** out) {
         d.Mns = p->Mns;
         d.gs = p->gs;
         d.S = p->S;
+        d.nflav = three ? 3 : 2;
+        if (three) {
+            d.vac3 = env->vac3.data();
+            d.fw6 = env->fw6.data();
+            std::memcpy(d.couplings6, env->cpl6, sizeof env->cpl6);
+        }
         *out = env.release();
     });
 }

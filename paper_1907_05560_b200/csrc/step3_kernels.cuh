@@ -1,0 +1,369 @@
+// 3-flavour stage kernels (BASELINE configs[1]; not in the reference, which
+// accepts Flvs = 2 only — DESIGN.md §9).  Same S1-S4 schedule, moments,
+// reductions and device control as the 2-flavour kernels (step_kernels.cuh);
+// what changes:
+//   * psi in C^3: species s = 2 f + pc (f = e, mu, tau; pc = particle class),
+//     6 components (re/im of e, mu, tau), state planes (s*6 + c);
+//   * work item = (particle class, cell): the three species of a class share
+//     the beam Hamiltonian, so one 3x3 propagator (su3_exp.cuh) per evolve
+//     serves three 3x3 complex mat-vecs;
+//   * rho = psi psi^dagger (9 reals); moments: 9 per geometric moment
+//     (single angle 9, bulb 18);
+//   * H_nu = H_vac(E) + diag(A,0,0) + H_nunu,
+//     H_nubar = conj(H_vac) - diag(A,0,0) - conj(H_nunu).
+#pragma once
+
+#include "step_kernels.cuh"
+#include "su3_exp.cuh"
+
+namespace oscb200 {
+
+constexpr int kNM3Max = 18;  // 9 x (a, b): single-angle and bulb geometries
+
+struct TrajRec3 {
+    double hb[4][9];   // beam part (H_nunu + matter) for H0..H3, particle convention
+    double dl[3];
+    double fold[2][2]; // (w, w n1)
+    double n1[3];      // cos theta' at r, r+dr/2, r+dr
+    double pad_;
+};
+
+// packed Hermitian helpers: index 0-2 diagonal, (3,4) 01, (5,6) 02, (7,8) 12
+__device__ __forceinline__ Herm3 herm_of(const double* v, const double* b, int pc) {
+    // particle: v + b ; antiparticle: conj(v) - conj(b)
+    // real parts v +- b; imaginary parts v_im + b_im (particle) or
+    // -v_im + b_im (antiparticle: conj(v) - conj(b))
+    Herm3 h;
+    const double sg = pc ? -1.0 : 1.0;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) h.d[k] = v[k] + sg * b[k];
+    h.o01 = Cx{v[3] + sg * b[3], sg * v[4] + b[4]};
+    h.o02 = Cx{v[5] + sg * b[5], sg * v[6] + b[6]};
+    h.o12 = Cx{v[7] + sg * b[7], sg * v[8] + b[8]};
+    return h;
+}
+
+__device__ __forceinline__ void apply3(const Mat3& U, const double (&x)[6], double (&y)[6]) {
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+        double re = 0.0, im = 0.0;
+#pragma unroll
+        for (int j = 0; j < 3; ++j) {
+            const Cx u = U.m[i][j];
+            re = fma(u.re, x[2 * j], fma(-u.im, x[2 * j + 1], re));
+            im = fma(u.re, x[2 * j + 1], fma(u.im, x[2 * j], im));
+        }
+        y[2 * i] = re;
+        y[2 * i + 1] = im;
+    }
+}
+
+// weighted rho = psi psi^dagger of the 3 species of a class, summed; for
+// antiparticles the row enters minus-conjugated (combine_species,
+// geometry.cpp:119-136) — folded into the signed weight g and an imaginary
+// sign flip.
+__device__ __forceinline__ void weighted_rho3(const double (&y)[3][6], const double (&g)[3], int pc,
+                                              double (&R)[9]) {
+#pragma unroll
+    for (int k = 0; k < 9; ++k) R[k] = 0.0;
+#pragma unroll
+    for (int f = 0; f < 3; ++f) {
+        const double ar = y[f][0], ai = y[f][1], br = y[f][2], bi = y[f][3], cr = y[f][4], ci = y[f][5];
+        const double gi = pc ? -g[f] : g[f];
+        R[0] += g[f] * (ar * ar + ai * ai);
+        R[1] += g[f] * (br * br + bi * bi);
+        R[2] += g[f] * (cr * cr + ci * ci);
+        R[3] += g[f] * (ar * br + ai * bi);  // a conj(b)
+        R[4] += gi * (ai * br - ar * bi);
+        R[5] += g[f] * (ar * cr + ai * ci);  // a conj(c)
+        R[6] += gi * (ai * cr - ar * ci);
+        R[7] += g[f] * (br * cr + bi * ci);  // b conj(c)
+        R[8] += gi * (bi * cr - br * ci);
+    }
+}
+
+template <int MODEL, int STAGE>
+__global__ void __launch_bounds__(kBlock, 1) k_stage3(StepArgs a) {
+    using Tr = StageTraits<STAGE>;
+    constexpr int NG = MODEL == 0 ? 1 : 2;  // geometric moments (a | a, b)
+    constexpr int NM = 9 * NG;
+    constexpr int NV = NM * Tr::nsets;
+    extern __shared__ __align__(128) unsigned char dsm3[];
+    __shared__ double tot[4][kNM3Max];
+    __shared__ double red[kWarps * (2 * kNM3Max + 1)];
+    __shared__ int is_last;
+
+    const Ctl* ctl = a.ctl;
+    grid_dependency_wait();
+    if (STAGE != 0 && (ctl->terminate || ctl->status)) return;
+    const int tid = threadIdx.x;
+    const int nb_half = gridDim.x / 2;
+    const int pc = blockIdx.x >= nb_half;
+    const int hb_ = blockIdx.x - pc * nb_half;
+    const int c0 = hb_ * a.chunk;
+    const int c1 = min(c0 + a.chunk, a.ncell);
+    const double r = ctl->r, dr = ctl->dr;
+    const double rk[3] = {r, r + 0.5 * dr, r + dr};
+    const int cur = ctl->cur;
+    const double* __restrict__ psi0 = a.psi0_buf[cur];
+    double* __restrict__ res = a.psi0_buf[cur ^ 1];
+    const size_t np = a.npad;
+    TrajRec3* rec = reinterpret_cast<TrajRec3*>(dsm3);
+
+    if (tid < 4 * NM) {
+        const int h = tid / NM, k = tid % NM;
+        if (Tr::hmask & (1 << h)) {
+            const int slot = h == 0 ? 0 : (h == 3 ? 2 : 1);
+            const int off = h == 2 ? 36 : 0;
+            // slot layout per set: 9 x geometric moment (a at 0..8, b at 9..17)
+            tot[h][k] = slot_total(a, slot, off + k);
+        }
+    }
+    if (STAGE == 0 && blockIdx.x == 0 && tid == 0) {
+        a.ctl->A[0] = matter_potential(a, rk[0]);
+        a.ctl->A[1] = matter_potential(a, rk[1]);
+        a.ctl->A[2] = matter_potential(a, rk[2]);
+    }
+    __syncthreads();
+    const double Am[3] = {STAGE ? ctl->A[0] : 0.0, STAGE ? ctl->A[1] : 0.0, STAGE ? ctl->A[2] : 0.0};
+    const int tr0 = c1 > c0 ? (int)div_e(c0, a.e_magic, a.e_shift) : 0;
+    const int ntr = c1 > c0 ? (int)div_e(c1 - 1, a.e_magic, a.e_shift) - tr0 + 1 : 0;
+    for (int i = tid; i < ntr; i += kBlock) {
+        const int traj = tr0 + i;
+        const int th = a.t_lo + traj / a.P;
+        Geo G[3];
+#pragma unroll
+        for (int q = 0; q < 3; ++q) G[q] = traj_geom<MODEL>(a, th, 0, rk[q]);
+        TrajRec3& R = rec[i];
+        R.dl[0] = (0.5 * dr) / (0.5 * (G[0].cdl + G[1].cdl));
+        R.dl[1] = (0.5 * dr) / (0.5 * (G[1].cdl + G[2].cdl));
+        R.dl[2] = dr / (0.5 * (G[0].cdl + G[2].cdl));
+#pragma unroll
+        for (int q = 0; q < 3; ++q) R.n1[q] = G[q].n[0];
+        const int fq[2] = {Tr::fold0, Tr::fold1};
+#pragma unroll
+        for (int f = 0; f < Tr::nsets; ++f) {
+            R.fold[f][0] = G[fq[f]].f[0];
+            R.fold[f][1] = G[fq[f]].f[1];
+        }
+        constexpr int hr[4] = {0, 2, 1, 2};
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+            if (!(Tr::hmask & (1 << h))) continue;
+            const int q = hr[h];
+            double D = 1.0;
+            if (MODEL == 0) {
+                const double ra = a.Rnu / rk[q], t = 1.0 - sqrt(1.0 - ra * ra);
+                D = 0.5 * t * t;
+            }
+#pragma unroll
+            for (int k = 0; k < 9; ++k)
+                R.hb[h][k] = MODEL == 0 ? tot[h][k] * D : tot[h][k] + tot[h][9 + k] * (-R.n1[q]);
+            R.hb[h][0] += Am[q];  // matter diag(A, 0, 0)
+        }
+    }
+    __syncthreads();
+
+    double acc[NV];
+#pragma unroll
+    for (int k = 0; k < NV; ++k) acc[k] = 0.0;
+    double emax = 0.0;
+    const bool stash = a.schedule == 1;
+
+    for (int cell = c0 + tid; cell < c1; cell += kBlock) {
+        const int traj = (int)div_e(cell, a.e_magic, a.e_shift);
+        const int e = cell - traj * a.E;
+        const TrajRec3& R = rec[traj - tr0];
+        double x[3][6];
+#pragma unroll
+        for (int f = 0; f < 3; ++f)
+#pragma unroll
+            for (int c = 0; c < 6; ++c) x[f][c] = __ldg(psi0 + (size_t)((2 * f + pc) * 6 + c) * np + cell);
+        double g[3];
+#pragma unroll
+        for (int f = 0; f < 3; ++f) g[f] = __ldg(a.g + (size_t)(2 * f + pc) * a.E + e);
+        double v[9];
+#pragma unroll
+        for (int k = 0; k < 9; ++k) v[k] = __ldg(a.vac3 + (size_t)e * 9 + k);
+        double Rr[9];
+        auto prop = [&](int h, int slot) { return exp_herm3(herm_of(v, R.hb[h], pc), R.dl[slot]); };
+
+        if (STAGE == 0) {
+            weighted_rho3(x, g, pc, Rr);
+#pragma unroll
+            for (int j = 0; j < NG; ++j)
+#pragma unroll
+                for (int k = 0; k < 9; ++k) acc[9 * j + k] += R.fold[0][j] * Rr[k];
+        } else if (STAGE == 2) {
+            const Mat3 um = prop(0, 0), uf = prop(0, 2);
+            double y[3][6];
+#pragma unroll
+            for (int f = 0; f < 3; ++f) apply3(um, x[f], y[f]);
+            weighted_rho3(y, g, pc, Rr);
+#pragma unroll
+            for (int j = 0; j < NG; ++j)
+#pragma unroll
+                for (int k = 0; k < 9; ++k) acc[NM + 9 * j + k] += R.fold[1][j] * Rr[k];
+#pragma unroll
+            for (int f = 0; f < 3; ++f) apply3(uf, x[f], y[f]);
+            weighted_rho3(y, g, pc, Rr);
+#pragma unroll
+            for (int j = 0; j < NG; ++j)
+#pragma unroll
+                for (int k = 0; k < 9; ++k) acc[9 * j + k] += R.fold[0][j] * Rr[k];
+        } else if (STAGE == 3) {
+            const Mat3 um = prop(0, 0), uh = prop(2, 1);
+            double hh[3][6];
+#pragma unroll
+            for (int f = 0; f < 3; ++f) {
+                double mid[6];
+                apply3(um, x[f], mid);
+                apply3(uh, mid, hh[f]);
+                if (stash)
+#pragma unroll
+                    for (int c = 0; c < 6; ++c) __stcg(a.half2 + (size_t)((2 * f + pc) * 6 + c) * np + cell, hh[f][c]);
+            }
+            weighted_rho3(hh, g, pc, Rr);
+#pragma unroll
+            for (int j = 0; j < NG; ++j)
+#pragma unroll
+                for (int k = 0; k < 9; ++k) acc[9 * j + k] += R.fold[0][j] * Rr[k];
+        } else {
+            double h2[3][6];
+            if (stash) {
+#pragma unroll
+                for (int f = 0; f < 3; ++f)
+#pragma unroll
+                    for (int c = 0; c < 6; ++c) h2[f][c] = __ldcg(a.half2 + (size_t)((2 * f + pc) * 6 + c) * np + cell);
+            } else {
+                const Mat3 um = prop(0, 0), uh = prop(2, 1);
+#pragma unroll
+                for (int f = 0; f < 3; ++f) {
+                    double mid[6];
+                    apply3(um, x[f], mid);
+                    apply3(uh, mid, h2[f]);
+                }
+            }
+            const Mat3 u3 = prop(3, 2);
+            double out[3][6];
+#pragma unroll
+            for (int f = 0; f < 3; ++f) {
+                double f3[6];
+                apply3(u3, x[f], f3);
+#pragma unroll
+                for (int c = 0; c < 6; ++c) {
+                    out[f][c] = (h2[f][c] + f3[c]) * 0.5;  // evolve_avg, beam.cpp:188-218
+                    res[(size_t)((2 * f + pc) * 6 + c) * np + cell] = out[f][c];
+                }
+            }
+            weighted_rho3(out, g, pc, Rr);
+#pragma unroll
+            for (int j = 0; j < NG; ++j)
+#pragma unroll
+                for (int k = 0; k < 9; ++k) acc[9 * j + k] += R.fold[0][j] * Rr[k];
+            const Mat3 u1 = prop(0, 2), u2 = prop(1, 2);
+#pragma unroll
+            for (int f = 0; f < 3; ++f) {
+                double f1[6], f2[6];
+                apply3(u1, x[f], f1);
+                apply3(u2, x[f], f2);
+#pragma unroll
+                for (int c = 0; c < 6; ++c) emax = fmax(emax, fabs((f1[c] + f2[c]) * 0.5 - out[f][c]));
+            }
+        }
+    }
+    grid_launch_dependents();
+
+    block_reduce<NV>(acc, emax, red);
+    if (tid == 0) {
+        double* p = a.partials + (size_t)blockIdx.x * kSlotDoubles;
+#pragma unroll
+        for (int k = 0; k < NV; ++k) p[k] = acc[k];
+        p[NV] = emax;
+        __threadfence();
+        const unsigned ticket = atomicAdd(&a.ctl->counter[Tr::slot], 1u);
+        is_last = ticket == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!is_last) return;
+    __threadfence();
+    double fv[NV];
+    double fm = 0.0;
+#pragma unroll
+    for (int k = 0; k < NV; ++k) fv[k] = 0.0;
+    for (int b = tid; b < (int)gridDim.x; b += kBlock) {
+        const double* p = a.partials + (size_t)b * kSlotDoubles;
+#pragma unroll
+        for (int k = 0; k < NV; ++k) fv[k] += __ldcg(p + k);
+        fm = fmax(fm, __ldcg(p + NV));
+    }
+    __syncthreads();
+    block_reduce<NV>(fv, fm, red);
+    __shared__ double fin[2 * kNM3Max + 1];
+    if (tid == 0) {
+#pragma unroll
+        for (int k = 0; k < NV; ++k) fin[k] = fv[k];
+        fin[NV] = fm;
+    }
+    __syncthreads();
+    if (tid < kSlotDoubles) {
+        // slot layout: per set 36 doubles (9 x up to 4 geometric moments),
+        // S2 = sums1 | sums2, S4 error at index 36
+        const int k = tid;
+        double v = 0.0;
+        if (STAGE == 2) {
+            if (k < 72) {
+                const int set = k / 36, j = k % 36;
+                v = j < NM ? fin[set * NM + j] : 0.0;
+            }
+        } else if (k < 36) {
+            v = k < NM ? fin[k] : 0.0;
+        } else if (k == 36) {
+            v = fin[NV];
+        }
+        a.xsend[(size_t)Tr::slot * kSlotDoubles + k] = v;
+        if (STAGE != 4 && !isfinite(v)) atomicOr(&a.ctl->bad_sums, 1);
+    }
+    if (tid == 0) a.ctl->counter[Tr::slot] = 0;
+    if (STAGE == 4 && a.fuse_ctl) {
+        __threadfence();
+        __syncthreads();
+        control_update(a, true);
+    }
+}
+
+inline size_t stage3_smem_bytes(int ntr_max) { return (size_t)ntr_max * sizeof(TrajRec3); }
+
+// 3-flavour init: pure flavour f = s / 2 plus eps noise on the other two
+// flavours, splitmix64-seeded by the global beam index j*6 + s (generalises
+// beam.cpp:41-57).
+__global__ void k_init3(StepArgs a, double eps) {
+    const int cell = blockIdx.x * blockDim.x + threadIdx.x;
+    if (cell >= a.ncell) return;
+    double* psi = a.psi0_buf[a.ctl->cur];
+    const int traj = cell / a.E, e = cell - traj * a.E;
+    const uint64_t j = (uint64_t)(a.t_lo * a.P + traj);
+    const size_t np = a.npad;
+    for (int s = 0; s < 6; ++s) {
+        const int f = s / 2;
+        double c[6] = {0, 0, 0, 0, 0, 0};
+        c[2 * f] = 1.0;
+        if (eps != 0.0) {
+            const uint64_t seed = j * 6 + s;
+            const int o1 = (f + 1) % 3, o2 = (f + 2) % 3;
+            const double u1 = eps * unit_noise(seed, e, 0), v1 = eps * unit_noise(seed, e, 1);
+            const double u2 = eps * unit_noise(seed, e, 2), v2 = eps * unit_noise(seed, e, 3);
+            const double q = __dsub_rn(__dsub_rn(__dsub_rn(__dsub_rn(1.0, __dmul_rn(u1, u1)), __dmul_rn(v1, v1)),
+                                                 __dmul_rn(u2, u2)),
+                                       __dmul_rn(v2, v2));
+            c[2 * f] = sqrt(fmax(0.0, q));
+            c[2 * o1] = u1;
+            c[2 * o1 + 1] = v1;
+            c[2 * o2] = u2;
+            c[2 * o2 + 1] = v2;
+        }
+        for (int k = 0; k < 6; ++k) psi[(size_t)(s * 6 + k) * np + cell] = c[k];
+    }
+}
+
+}  // namespace oscb200

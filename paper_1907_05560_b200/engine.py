@@ -98,6 +98,17 @@ class Environment:
         p.matter_profile = cfg.matter_id
         p.Ye, p.nb0, p.hNS, p.Mns, p.gs, p.S = (v["Ye"], v["nb0"], v["hNS"], v["Mns"], v["gs"],
                                                  v["S"])
+        p.nflav = v["Flvs"]
+        if p.nflav == 3:
+            prov = cfg.provided
+            p.dm2 = v["dm2_21"] if "dm2_21" in prov else v["dm2"]
+            p.theta = v["theta12"] if "theta12" in prov else v["theta"]
+            p.dm2_31, p.theta13, p.theta23, p.delta_cp = (v["dm2_31"], v["theta13"],
+                                                           v["theta23"], v["deltaCP"])
+            for arr, name in ((p.L_tau, "L"), (p.T_tau, "T"), (p.Emean_tau, "E"),
+                              (p.eta_tau, "eta")):
+                for i, x in enumerate(cfg.tau(name)):
+                    arr[i] = x
         self.cfg = cfg
         self._h = C.c_void_p()
         check(lib().osc_env_build(C.byref(p), C.byref(self._h)))
@@ -107,6 +118,9 @@ class Environment:
         self.emean = list(emean)
         d = self.desc
         self.model, self.abins, self.pbins, self.ebins = d.model, d.abins, d.pbins, d.ebins
+        self.nflav = 3 if d.nflav == 3 else 2
+        self.species_count = 6 if self.nflav == 3 else 4
+        self.comps = 6 if self.nflav == 3 else 4
 
     @classmethod
     def from_config(cls, cfg: RunConfig) -> "Environment":
@@ -122,10 +136,14 @@ class Environment:
         d = self.desc
         T, P, E = d.abins, d.pbins, d.ebins
         arr = lambda p, n: np.ctypeslib.as_array(p, shape=(n,)).copy()
-        return dict(cos2=arr(d.cos2_theta0, T), sin0=arr(d.sin_theta0, T),
-                    cphi=arr(d.cos_phi, P), sphi=arr(d.sin_phi, P), vac11=arr(d.vac_h11, E),
-                    vac12=arr(d.vac_h12, E), fw=arr(d.fw, 4 * E).reshape(4, E),
-                    couplings=np.array(list(d.couplings)), emean=np.array(self.emean))
+        t = dict(cos2=arr(d.cos2_theta0, T), sin0=arr(d.sin_theta0, T),
+                 cphi=arr(d.cos_phi, P), sphi=arr(d.sin_phi, P), vac11=arr(d.vac_h11, E),
+                 vac12=arr(d.vac_h12, E), fw=arr(d.fw, 4 * E).reshape(4, E),
+                 couplings=np.array(list(d.couplings)), emean=np.array(self.emean))
+        if self.nflav == 3:
+            t.update(vac3=arr(d.vac3, 9 * E).reshape(E, 9), fw6=arr(d.fw6, 6 * E).reshape(6, E),
+                     couplings6=np.array(list(d.couplings6)))
+        return t
 
     @property
     def trajectories(self) -> int:

@@ -21,7 +21,8 @@ class OscDesc(C.Structure):
                 ("vac_h11", _dp), ("vac_h12", _dp), ("fw", _dp),
                 ("couplings", C.c_double * 4), ("perturb", C.c_double),
                 ("matter_profile", C.c_int), ("Ye", C.c_double), ("nb0", C.c_double),
-                ("hNS", C.c_double), ("Mns", C.c_double), ("gs", C.c_double), ("S", C.c_double)]
+                ("hNS", C.c_double), ("Mns", C.c_double), ("gs", C.c_double), ("S", C.c_double),
+                ("nflav", C.c_int), ("vac3", _dp), ("fw6", _dp), ("couplings6", C.c_double * 6)]
 
 
 class OscComm(C.Structure):
@@ -58,7 +59,11 @@ class OscParams(C.Structure):
                 ("perturb", C.c_double), ("L", C.c_double * 4), ("T", C.c_double * 4),
                 ("Emean", C.c_double * 4), ("eta", C.c_double * 4),
                 ("matter_profile", C.c_int), ("Ye", C.c_double), ("nb0", C.c_double),
-                ("hNS", C.c_double), ("Mns", C.c_double), ("gs", C.c_double), ("S", C.c_double)]
+                ("hNS", C.c_double), ("Mns", C.c_double), ("gs", C.c_double), ("S", C.c_double),
+                ("nflav", C.c_int), ("dm2_31", C.c_double), ("theta13", C.c_double),
+                ("theta23", C.c_double), ("delta_cp", C.c_double), ("L_tau", C.c_double * 2),
+                ("T_tau", C.c_double * 2), ("Emean_tau", C.c_double * 2),
+                ("eta_tau", C.c_double * 2)]
 
 
 # Every symbol the header declares (checked by tests/test_abi.py).

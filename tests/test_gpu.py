@@ -356,3 +356,56 @@ def test_plane_cylinder_literal_step_sizes(pyoracle, name):
     # (as for the literal bulb configs), so only a loose bound
     d = np.max(np.abs(eng.state() - o.get_state()))
     assert np.isfinite(eng.state()).all() and d <= 1e-3, d
+
+
+# ------------------------------------------------------ 3 flavours (configs[1])
+def rho3(mode1, ntraj, E):
+    x = mode1.reshape(ntraj, 6, 6, E)
+    psi = x[:, :, 0::2] + 1j * x[:, :, 1::2]  # [traj][s][flavour][e]
+    return np.einsum("tsie,tsje->tsije", psi, psi.conj()), (abs(psi) ** 2).sum(axis=2)
+
+
+def test_three_flavour_matches_oracle(pyoracle):
+    """configs[1] physics on a reduced grid in a resolved window: GPU (closed-
+    form SU(3) propagator) vs the C restatement (series exponential)."""
+    cfg = baseline_config("configs1", Abins=16, Ebins=12, R0=50, Rn=51, dr=1e-6, max_dr=1e-6,
+                          Ts=20)
+    env, eng = make(cfg)
+    o = pyoracle.Oracle3(cfg)
+    assert np.array_equal(eng.state(), o.get_state())  # seeded 3-flavour init
+    s = eng.run(StepControl.from_config(cfg))
+    so = o.run()
+    assert s.iterations == so["iterations"] == 20
+    (rg, tg), (ro, _) = rho3(eng.state(), 16, 12), rho3(o.get_state(), 16, 12)
+    assert np.abs(rg - ro).max() <= RHO_TOL
+    assert np.abs(tg - 1.0).max() <= TRACE_TOL
+    env2, fresh = make(cfg)
+    e_gpu = fresh.trial_step_error(60.0, 1e-5)
+    e_orc = pyoracle.Oracle3(cfg).trial_step(60.0, 1e-5)
+    assert e_gpu == pytest.approx(e_orc, rel=1e-6)
+
+
+def test_three_flavour_decoupled_tau_equals_two_flavour_gpu():
+    """theta13 = theta23 = 0 and a dark tau sector: the 3-flavour kernels'
+    e-mu densities equal the 2-flavour kernels' (both on the GPU)."""
+    kw = dict(Abins=12, Ebins=16, R0=50, Rn=51, dr=2e-4, max_dr=2e-4, Ts=15)
+    c2 = baseline_config("configs0", **kw)
+    c3 = baseline_config("configs1", **kw)
+    for kv in ("dm2_21=-2.35e-3", "theta12=0.1", "theta13=0", "theta23=0", "dm2_31=-2.4e-3",
+               "Lvtau=0", "Lvatau=0", "hasMatter=0"):
+        c3.override(kv)
+    env2, e2 = make(c2)
+    env3, e3 = make(c3)
+    s2 = e2.state().reshape(12, 4, 4, 16)
+    s3 = np.zeros((12, 6, 6, 16))
+    s3[:, :4, :4] = s2
+    s3[:, 4, 4] = s3[:, 5, 4] = 1.0
+    e3.set_state(s3.ravel())
+    e2.run(StepControl.from_config(c2))
+    e3.run(StepControl.from_config(c3))
+    a = e2.state().reshape(12, 4, 4, 16)
+    x = e3.state().reshape(12, 6, 6, 16)[:, :4]
+    pa, pb = a[:, :, 0] + 1j * a[:, :, 1], a[:, :, 2] + 1j * a[:, :, 3]
+    qa, qb = x[:, :, 0] + 1j * x[:, :, 1], x[:, :, 2] + 1j * x[:, :, 3]
+    assert np.abs((abs(pa) ** 2 - abs(pb) ** 2) - (abs(qa) ** 2 - abs(qb) ** 2)).max() <= 1e-12
+    assert np.abs(pa * pb.conj() - qa * qb.conj()).max() <= 1e-12
