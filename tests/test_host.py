@@ -68,9 +68,11 @@ def test_config_parse_and_validation():
         cfg.require_runnable()  # physics keys missing
     c = baseline_config("configs0")
     c.require_runnable()
-    c.override("Flvs=3")
+    c.override("Flvs=4")
     with pytest.raises(ConfigError):
         c.require_runnable()
+    c.override("Flvs=3")
+    c.require_runnable()  # 3 flavours: sa / bulb (configs[1])
 
 
 def test_baseline_configs_shapes():

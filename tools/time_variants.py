@@ -11,7 +11,7 @@ import os, sys, time
 sys.path.insert(0, %r)
 from paper_1907_05560_b200 import *
 out = []
-for name, n in (("configs2", 64), ("configs0", 256), ("configs3", 64), ("configs4", 64)):
+for name, n in (("configs2", 64), ("configs0", 256), ("configs1", 128), ("configs3", 64), ("configs4", 64)):
     cfg = baseline_config(name)
     env = Environment.from_config(cfg); eng = Engine(env); eng.init_states()
     for sched in (0, 1):
