@@ -48,6 +48,7 @@ def _args():
     ap.add_argument("--schedule", type=int, default=-1)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-steps", type=int, default=0)
+    ap.add_argument("--no-other-configs", action="store_true")
     return ap.parse_args()
 
 
@@ -290,6 +291,11 @@ def main():
                          "hbm_compulsory_gbs": 256 * cells_total / (ms / a.steps * 1e-3) / 1e9,
                          "hbm_peak_gbs": hbm_peak[0], "hbm_peak_source": hbm_peak[1]}}
 
+    others = None
+    if world == 1 and not a.no_other_configs:
+        others = {name: _other_config(name, local, a.no_cpu_baseline)
+                  for name in ("configs0", "configs1", "configs3", "configs4") if name != a.config}
+
     cpu = None
     if rank == 0 and world == 1 and not a.no_cpu_baseline:
         try:
@@ -322,11 +328,62 @@ def main():
             "clocks": clocks,
             "roofline": roof,
             "cpu_baseline": cpu,
+            "other_configs": others,
         }
         print(json.dumps(line), flush=True)
     eng.close()
     if dist is not None:
         dist.destroy_process_group()
+
+
+def _other_config(name: str, device: int, no_cpu: bool) -> dict:
+    """Device-resident throughput of another BASELINE config (same method as
+    `value`), plus its CPU baseline: the reference engine for configs[0], the C
+    restatement (1 thread, parity unpinned) for configs[1]/[3]/[4], which the
+    reference does not implement."""
+    import torch
+
+    from paper_1907_05560_b200 import Engine, Environment, StepControl, baseline_config
+
+    cfg = baseline_config(name)
+    env = Environment.from_config(cfg)
+    eng = Engine(env, device=device)
+    eng.init_states()
+    ctl = StepControl.from_config(cfg)
+    ctl.Ts, ctl.Rn = 0, 1e9
+    stream = torch.cuda.ExternalStream(eng.stream())
+    steps = 200 if env.cells < 200000 else 60
+    eng.begin(ctl)
+    eng.enqueue_steps(5)
+    eng.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    eng.enqueue_steps(steps)
+    e1.record(stream)
+    e1.synchronize()
+    ms = e0.elapsed_time(e1)
+    q = eng.query()
+    eng.close()
+    out = {"value": env.cells * steps / (ms * 1e-3), "unit": UNIT, "ms_per_step": ms / steps,
+           "cells": env.cells, "flavours": env.nflav, "steps_timed": steps, "status": q["status"]}
+    if no_cpu:
+        return out
+    try:
+        if name == "configs0":
+            r = cpu_reference(cfg, 20, 1)
+            out["cpu"] = {"value": r["value"], "cores": r["cores"], "kind": "reference",
+                          "sample": "20 fixed steps, reference engine"}
+        else:
+            po = _ref_lib()
+            o = po.Oracle3(cfg) if env.nflav == 3 else po.Oracle(cfg)
+            t0 = time.perf_counter()
+            o.run(ts=1)
+            wall = time.perf_counter() - t0
+            out["cpu"] = {"value": env.cells / wall, "cores": 1, "kind": "port",
+                          "sample": "1 step, C restatement (not in the reference; parity unpinned)"}
+    except Exception as e:  # noqa: BLE001
+        out["cpu"] = {"value": None, "sample": f"unavailable: {type(e).__name__}: {e}"}
+    return out
 
 
 def _hbm_peak():
