@@ -224,9 +224,11 @@ def main():
     eng.synchronize()
     barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    n_launch0 = eng.launch_count()
     e0.record(stream)
     eng.enqueue_steps(a.steps)
     e1.record(stream)
+    n_launch = eng.launch_count() - n_launch0
     e1.synchronize()
     barrier()
     ms = max_over_ranks(e0.elapsed_time(e1))
@@ -324,7 +326,7 @@ def main():
                     "d2h_bytes_per_step": bytes_state / e2e_steps,
                     "call": "osc_set_state(host) + osc_run(Ts=K) + osc_get_state(host)",
                     "steps": int(summ.iterations), "ms": ms_e2e},
-            "gpu_launches": eng.launches_per_step() * a.steps,
+            "gpu_launches": n_launch,
             "clocks": clocks,
             "roofline": roof,
             "cpu_baseline": cpu,

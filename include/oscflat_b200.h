@@ -177,6 +177,17 @@ int osc_debug_sums(OscCtx* ctx, double* out60);
 /* Configure the stage schedule: 0 = recompute intermediates from psi0,
  * 1 = stash half2 in HBM between S3 and S4. */
 int osc_set_schedule(OscCtx* ctx, int schedule);
+/* on=1: multi-step batches on a single-GPU 2-flavour context run as ONE
+ * persistent cooperative kernel (grid barriers instead of kernel boundaries;
+ * opt-in, also via env OSC_PERSIST=1).  on=0 (default): per-stage kernels
+ * with programmatic dependent launch in a CUDA graph of 8 steps.  Returns
+ * OSC_ERR_CONFIG when the persistent kernel is unavailable for this context. */
+int osc_set_persistent(OscCtx* ctx, int on);
+/* 1 if multi-step batches currently use the persistent kernel. */
+int osc_get_persistent(OscCtx* ctx);
+/* Number of kernels this context has launched so far (graph launches count
+ * every kernel node) — the bench's gpu_launches evidence. */
+unsigned long long osc_launch_count(const OscCtx* ctx);
 
 /* Measured FP64 FMA throughput (thread-level DFMA instructions per second)
  * from a DFMA-chain microkernel on `device` — the FP64 roofline denominator. */

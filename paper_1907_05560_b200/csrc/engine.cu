@@ -10,6 +10,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -105,6 +106,17 @@ StageFn stage3_fn(int stage) {
         default: return k_stage3<MODEL, 4>;
     }
 }
+using PersistFn = void (*)(StepArgs, int);
+PersistFn persist_kernel(int model) {
+    switch (model) {
+        case 0: return k_persist<0>;
+        case 1: return k_persist<1>;
+        case 2: return k_persist<2>;
+        case 3: return k_persist<3>;
+        default: return k_persist<4>;
+    }
+}
+
 StageFn stage_kernel(int nflav, int model, int stage) {
     if (nflav == 3) return model == 0 ? stage3_fn<0>(stage) : stage3_fn<1>(stage);
     switch (model) {
@@ -150,6 +162,15 @@ struct OscCtx {
     int nplanes = 16;  // state planes per buffer
     DevBuf<double> vac3;
     int use_pdl = 1;
+    int persist_ok = 0;  // the persistent kernel fits one resident wave
+    int persist = 0;     // multi-step batches use the persistent kernel
+    unsigned long long nlaunch = 0;  // kernels this context launched
+    bool capturing = false;
+    int graph_kernels = 0;
+    void count(int k = 1) {
+        if (capturing) graph_kernels += k;
+        else nlaunch += k;
+    }
     cudaStream_t stream = nullptr;
     nccl::Comm comm = nullptr;
 
@@ -191,6 +212,7 @@ struct OscCtx {
         cfg.attrs = attr;
         cfg.numAttrs = 1;
         CUDA_OK(cudaLaunchKernelEx(&cfg, fn, args));
+        count();
     }
 
     void exchange(int slot) {
@@ -212,6 +234,7 @@ struct OscCtx {
         exchange(3);
         if (nranks > 1) {
             k_control<<<1, 128, 0, stream>>>(args);
+            count();
             CUDA_OK(cudaGetLastError());
         }
     }
@@ -228,17 +251,50 @@ struct OscCtx {
         }
         cudaGraph_t g_ = nullptr;
         CUDA_OK(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
+        capturing = true;
+        graph_kernels = 0;
         for (int i = 0; i < steps; ++i) enqueue_step();
+        capturing = false;
         CUDA_OK(cudaStreamEndCapture(stream, &g_));
         CUDA_OK(cudaGraphInstantiate(&graph, g_, 0));
         cudaGraphDestroy(g_);
         graph_steps = steps;
     }
 
+    size_t persist_smem() const {
+        size_t m = 0;
+        for (int st : {2, 3, 4}) m = std::max(m, stage_smem_bytes(st, schedule, ntr_max));
+        return m;
+    }
+
+    // n steps in ONE cooperative launch: grid barriers replace the kernel
+    // boundaries (single GPU; every block resident by construction).
+    void launch_persist(int n) {
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(nblocks);
+        cfg.blockDim = dim3(kBlock);
+        cfg.dynamicSmemBytes = persist_smem();
+        cfg.stream = stream;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeCooperative;
+        attr[0].val.cooperative = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        CUDA_OK(cudaLaunchKernelEx(&cfg, persist_kernel(desc.model), args, n));
+        count();
+    }
+
     void enqueue_steps(int n) {
+        if (persist && n > 1) {
+            launch_persist(n);
+            return;
+        }
         if (n >= 8) {
             if (!graph) build_graph(8);
-            for (; n >= graph_steps; n -= graph_steps) CUDA_OK(cudaGraphLaunch(graph, stream));
+            for (; n >= graph_steps; n -= graph_steps) {
+                CUDA_OK(cudaGraphLaunch(graph, stream));
+                nlaunch += graph_kernels;
+            }
         }
         for (; n > 0; --n) enqueue_step();
     }
@@ -457,6 +513,20 @@ int osc_create(const OscDesc* desc, const OscComm* comm, OscCtx** out) {
         }
         c->partials.alloc((size_t)c->nblocks * kSlotDoubles);
 
+        // persistent kernel: single GPU, 2 flavours, one resident wave
+        if (c->nranks == 1 && c->nflav == 2) {
+            const PersistFn pf = persist_kernel(desc->model);
+            const size_t sm = c->persist_smem();
+            CUDA_OK(cudaFuncSetAttribute(pf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+            int per_sm = 0;
+            CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pf, kBlock, sm));
+            c->persist_ok = (long)per_sm * c->nsm >= c->nblocks && OSC_DEBUG_MODE == 0;
+            // opt-in (OSC_PERSIST=1 or osc_set_persistent): measured slower
+            // than the PDL-pipelined stage kernels on every BASELINE config
+            const char* env = std::getenv("OSC_PERSIST");
+            c->persist = c->persist_ok && env && env[0] == '1';
+        }
+
         if (c->nranks > 1) {
             if (!comm->nccl_unique_id) throw Error(OSC_ERR_PARALLEL, "osc_create: missing NCCL unique id");
             nccl::UniqueId id;
@@ -542,6 +612,7 @@ int osc_init_states(OscCtx* c) {
             k_init3<<<(c->ncell + 255) / 256, 256, 0, c->stream>>>(c->args, c->desc.perturb);
         else
             k_init<<<(c->ncell + 255) / 256, 256, 0, c->stream>>>(c->args, c->desc.perturb);
+        c->count();
         CUDA_OK(cudaGetLastError());
         CUDA_OK(cudaStreamSynchronize(c->stream));
     });
@@ -553,7 +624,7 @@ static void set_state_impl(OscCtx* c, const double* src, size_t n, cudaMemcpyKin
     CUDA_OK(cudaSetDevice(c->device));
     if (c->staging.n < want) c->staging.alloc(want);
     CUDA_OK(cudaMemcpyAsync(c->staging.p, src, want * sizeof(double), kind, c->stream));
-    k_unpack<<<c->nsm * 8, 256, 0, c->stream>>>(c->args, c->staging.p, want);
+    k_unpack<<<c->nsm * 8, 256, 0, c->stream>>>(c->args, c->staging.p, want); c->count();
     CUDA_OK(cudaGetLastError());
     CUDA_OK(cudaStreamSynchronize(c->stream));
 }
@@ -563,7 +634,7 @@ static void get_state_impl(OscCtx* c, double* dst, size_t n, cudaMemcpyKind kind
     if (n != want) throw Error(OSC_ERR_IO, "extract_mode1: payload size mismatch");
     CUDA_OK(cudaSetDevice(c->device));
     if (c->staging.n < want) c->staging.alloc(want);
-    k_pack<<<c->nsm * 8, 256, 0, c->stream>>>(c->args, c->staging.p, want);
+    k_pack<<<c->nsm * 8, 256, 0, c->stream>>>(c->args, c->staging.p, want); c->count();
     CUDA_OK(cudaGetLastError());
     CUDA_OK(cudaMemcpyAsync(dst, c->staging.p, want * sizeof(double), kind, c->stream));
     CUDA_OK(cudaStreamSynchronize(c->stream));
@@ -674,12 +745,27 @@ int osc_set_schedule(OscCtx* c, int schedule) {
         c->schedule = schedule;
         c->args.schedule = schedule;
         c->args.half2 = c->half2.p;
+        if (c->persist_ok)
+            CUDA_OK(cudaFuncSetAttribute(persist_kernel(c->desc.model), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)c->persist_smem()));
         if (c->graph) {
             cudaGraphExecDestroy(c->graph);
             c->graph = nullptr;
         }
     });
 }
+
+int osc_set_persistent(OscCtx* c, int on) {
+    return guarded([&] {
+        if (on && !c->persist_ok)
+            throw Error(OSC_ERR_CONFIG, "persistent kernel unavailable (multi-rank, 3 flavours or occupancy)");
+        c->persist = on ? 1 : 0;
+    });
+}
+
+int osc_get_persistent(OscCtx* c) { return c ? c->persist : 0; }
+
+unsigned long long osc_launch_count(const OscCtx* c) { return c ? c->nlaunch : 0; }
 
 int osc_fp64_peak(int device, double* dfma_per_s, double* ms_out) {
     return guarded([&] {
@@ -743,7 +829,7 @@ int osc_max_norm_dev(OscCtx* c, double* out) {
     return guarded([&] {
         CUDA_OK(cudaSetDevice(c->device));
         CUDA_OK(cudaMemsetAsync(c->scratch.p, 0, sizeof(unsigned long long), c->stream));
-        k_norm_dev<<<c->nsm * 4, 256, 0, c->stream>>>(c->args, c->scratch.p);
+        k_norm_dev<<<c->nsm * 4, 256, 0, c->stream>>>(c->args, c->scratch.p); c->count();
         CUDA_OK(cudaGetLastError());
         unsigned long long bits = 0;
         CUDA_OK(cudaMemcpyAsync(&bits, c->scratch.p, sizeof bits, cudaMemcpyDeviceToHost, c->stream));

@@ -277,6 +277,19 @@ class Engine:
     def set_schedule(self, schedule: int) -> None:
         check(lib().osc_set_schedule(self._ctx, schedule))
 
+    def set_persistent(self, on: bool) -> None:
+        """Multi-step batches as one persistent cooperative kernel (default
+        where available) or as per-stage kernels in a CUDA graph."""
+        check(lib().osc_set_persistent(self._ctx, 1 if on else 0))
+
+    @property
+    def persistent(self) -> bool:
+        return bool(lib().osc_get_persistent(self._ctx))
+
+    def launch_count(self) -> int:
+        """Kernels this engine has launched so far (graph nodes included)."""
+        return int(lib().osc_launch_count(self._ctx))
+
 
 def fp64_peak(device: int = 0) -> float:
     """Thread-level DFMA instructions per second measured on `device`."""

@@ -14,7 +14,7 @@ import os
 import numpy as np
 import pytest
 
-from paper_1907_05560_b200 import (Engine, Environment, NumericError, StepControl,
+from paper_1907_05560_b200 import (ConfigError, Engine, Environment, NumericError, StepControl,
                                    baseline_config, parse_config)
 
 pytestmark = pytest.mark.gpu
@@ -409,3 +409,34 @@ def test_three_flavour_decoupled_tau_equals_two_flavour_gpu():
     qa, qb = x[:, :, 0] + 1j * x[:, :, 1], x[:, :, 2] + 1j * x[:, :, 3]
     assert np.abs((abs(pa) ** 2 - abs(pb) ** 2) - (abs(qa) ** 2 - abs(qb) ** 2)).max() <= 1e-12
     assert np.abs(pa * pb.conj() - qa * qb.conj()).max() <= 1e-12
+
+
+@pytest.mark.parametrize("model", ["sa", "bulb", "ebulb", "plane", "cylinder"])
+def test_persistent_kernel_bit_identical_to_stage_kernels(model):
+    """The persistent cooperative kernel (grid barriers) and the per-stage
+    kernels (CUDA graph) run the same reductions in the same order: states,
+    step sequence and counters must agree bit for bit, rejections included."""
+    base = {"sa": "configs0", "bulb": "configs0", "ebulb": "configs0", "plane": "configs3",
+            "cylinder": "configs4"}[model]
+    cfg = baseline_config(base, Abins=24, Ebins=20, Ts=40, dr=0.5, max_dr=0.5, eps0=1e-9)
+    if model in ("sa", "ebulb"):
+        cfg.override(f"model={model}")
+    if model == "ebulb":
+        cfg.override("Pbins=8").override("perturb=1e-6")
+    if base != "configs0":
+        cfg.override("Pbins=8")
+    out = []
+    for on in (True, False):
+        env, eng = make(cfg)
+        try:
+            eng.set_persistent(on)
+        except ConfigError:
+            pytest.skip("persistent kernel unavailable on this device")
+        n0 = eng.launch_count()
+        s = eng.run(StepControl.from_config(cfg))
+        out.append((s.iterations, s.accepted, s.rejected, s.final_r, eng.state(), eng.launch_count() - n0))
+    (ia, aa, ra, fa, sa_, la), (ib, ab, rb, fb, sb, lb) = out
+    assert (ia, aa, ra, fa) == (ib, ab, rb, fb)
+    assert ia == 40 and ra > 0
+    assert np.array_equal(sa_, sb)
+    assert la < lb  # one launch per batch instead of three per step

@@ -22,7 +22,7 @@ def header_symbols():
     for f in os.listdir(os.path.join(ROOT, "include")):
         if f.endswith(".h"):
             txt = open(os.path.join(ROOT, "include", f)).read()
-            syms |= set(re.findall(r"^\s*(?:int|double|void\s*\*|const char\s*\*|void)\s+(osc_\w+)\s*\(",
+            syms |= set(re.findall(r"^\s*(?:int|double|unsigned long long|void\s*\*|const char\s*\*|void)\s+(osc_\w+)\s*\(",
                                    txt, flags=re.M))
     return syms
 

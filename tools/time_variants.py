@@ -14,15 +14,19 @@ out = []
 for name, n in (("configs2", 64), ("configs0", 256), ("configs1", 128), ("configs3", 64), ("configs4", 64)):
     cfg = baseline_config(name)
     env = Environment.from_config(cfg); eng = Engine(env); eng.init_states()
-    for sched in (0, 1):
+    for sched, pers in ((1, 1), (1, 0), (0, 1)):
         eng.set_schedule(sched)
+        try:
+            eng.set_persistent(bool(pers))
+        except Exception:
+            continue
         ctl = StepControl.from_config(cfg); ctl.Rn = 1e9; ctl.Ts = 0
         eng.begin(ctl); eng.enqueue_steps(16); eng.synchronize()
         best = 1e9
         for rep in range(3):
             t = time.perf_counter(); eng.enqueue_steps(n); eng.synchronize(); best = min(best, time.perf_counter() - t)
         st = eng.profile_stages(10)
-        out.append(f"{name} s{sched}: {best/n*1e6:7.1f} us/step  {env.cells*n/best:.3e}/s  stages " + " ".join(f"{x*1e3:6.1f}" for x in st))
+        out.append(f"{name} s{sched}p{pers}: {best/n*1e6:7.1f} us/step  {env.cells*n/best:.3e}/s  stages " + " ".join(f"{x*1e3:6.1f}" for x in st))
 print("\n".join(out))
 ''' % ROOT
 
