@@ -157,7 +157,7 @@ struct OscCtx {
     int ntraj = 0, ncell = 0, npad = 0;
     int nsm = 0, nblocks = 0, chunk = 0, ntr_max = 0;
     uint32_t e_magic = 0, e_shift = 0;
-    int schedule = 1;  // 1: stash half2 (default), 0: recompute it in S4
+    int schedule = 1;  // 1: S3 stashes propagators for S4 (default), 0: S4 recomputes them
     int nflav = 2;
     int nplanes = 16;  // state planes per buffer
     DevBuf<double> vac3;
@@ -175,7 +175,7 @@ struct OscCtx {
     nccl::Comm comm = nullptr;
 
     DevBuf<double> cos2, sin0, cphi, sphi, vac11, vac12, g;
-    DevBuf<double> psi[2], half2, xbuf, xsend, partials, staging;
+    DevBuf<double> psi[2], stash, xbuf, xsend, partials, staging;
     DevBuf<Ctl> ctl;
     DevBuf<unsigned long long> scratch;
     Ctl* h_ctl = nullptr;  // pinned mirror
@@ -550,7 +550,7 @@ int osc_create(const OscDesc* desc, const OscComm* comm, OscCtx** out) {
         a.e_magic = c->e_magic;
         a.e_shift = c->e_shift;
         a.schedule = c->schedule;
-        c->half2.alloc((size_t)c->npad * c->nplanes);
+        c->stash.alloc((size_t)c->npad * c->nplanes);
         a.Rnu = desc->Rnu;
         a.dcos2 = 1.0 / c->T;
         a.phi_measure = desc->model >= OSC_MODEL_EXT_BULB ? 1.0 / c->P : 1.0;
@@ -577,7 +577,7 @@ int osc_create(const OscDesc* desc, const OscComm* comm, OscCtx** out) {
         a.S = desc->S;
         a.psi0_buf[0] = c->psi[0].p;
         a.psi0_buf[1] = c->psi[1].p;
-        a.half2 = c->half2.p;
+        a.stash = c->stash.p;
         a.xbuf = c->xbuf.p;
         a.xsend = c->nranks > 1 ? c->xsend.p : c->xbuf.p;
         a.partials = c->partials.p;
@@ -741,10 +741,10 @@ int osc_set_schedule(OscCtx* c, int schedule) {
     return guarded([&] {
         CUDA_OK(cudaSetDevice(c->device));
         if (schedule != 0 && schedule != 1) throw Error(OSC_ERR_CONFIG, "schedule must be 0 or 1");
-        if (schedule == 1 && !c->half2.p) c->half2.alloc((size_t)c->npad * c->nplanes);
+        if (schedule == 1 && !c->stash.p) c->stash.alloc((size_t)c->npad * c->nplanes);
         c->schedule = schedule;
         c->args.schedule = schedule;
-        c->args.half2 = c->half2.p;
+        c->args.stash = c->stash.p;
         if (c->persist_ok)
             CUDA_OK(cudaFuncSetAttribute(persist_kernel(c->desc.model), cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)c->persist_smem()));

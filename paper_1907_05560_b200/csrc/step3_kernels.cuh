@@ -221,7 +221,7 @@ __global__ void __launch_bounds__(kBlock, 1) k_stage3(StepArgs a) {
                 apply3(uh, mid, hh[f]);
                 if (stash)
 #pragma unroll
-                    for (int c = 0; c < 6; ++c) __stcg(a.half2 + (size_t)((2 * f + pc) * 6 + c) * np + cell, hh[f][c]);
+                    for (int c = 0; c < 6; ++c) __stcg(a.stash + (size_t)((2 * f + pc) * 6 + c) * np + cell, hh[f][c]);
             }
             weighted_rho3(hh, g, pc, Rr);
 #pragma unroll
@@ -234,7 +234,7 @@ __global__ void __launch_bounds__(kBlock, 1) k_stage3(StepArgs a) {
 #pragma unroll
                 for (int f = 0; f < 3; ++f)
 #pragma unroll
-                    for (int c = 0; c < 6; ++c) h2[f][c] = __ldcg(a.half2 + (size_t)((2 * f + pc) * 6 + c) * np + cell);
+                    for (int c = 0; c < 6; ++c) h2[f][c] = __ldcg(a.stash + (size_t)((2 * f + pc) * 6 + c) * np + cell);
             } else {
                 const Mat3 um = prop(0, 0), uh = prop(2, 1);
 #pragma unroll
