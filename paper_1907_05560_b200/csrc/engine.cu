@@ -487,24 +487,41 @@ int osc_create(const OscDesc* desc, const OscComm* comm, OscCtx** out) {
 
         // Launch geometry: one resident wave of blocks (2 per SM, the
         // __launch_bounds__ target), half of them per particle class; each
-        // block owns a contiguous, warp-aligned chunk of cells.
+        // block owns a contiguous, warp-aligned chunk of cells.  When the
+        // per-trajectory records of a chunk would push a block's shared
+        // memory past what two resident blocks per SM allow (few energy bins
+        // per trajectory: the cylinder model), the grid doubles (two waves of
+        // half-size chunks) instead of running at half occupancy.
         {
             const int occ = OSC_MIN_BLOCKS;
-            const int nb = std::max(1, c->nsm * occ);
-            // 3 flavours: blocks split in halves by particle class
-            const int per = c->nflav == 3 ? nb / 2 : nb;
-            int chunk = (c->ncell + per - 1) / per;
-            chunk = std::max(32, (chunk + 31) / 32 * 32);
-            c->nblocks = c->nflav == 3 ? 2 * per : nb;
-            c->chunk = chunk;
-            c->ntr_max = chunk / c->E + 2;
-            const size_t smax =
-                c->nflav == 3 ? stage3_smem_bytes(c->ntr_max) : stage_smem_bytes(4, 1, c->ntr_max);
-            if (smax > 200 * 1024)
-                throw Error(OSC_ERR_CONFIG, "osc_create: trajectory records exceed shared memory");
-            for (int st : {0, 2, 3, 4})
-                CUDA_OK(cudaFuncSetAttribute(stage_kernel(c->nflav, desc->model, st),
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smax));
+            int nb = std::max(1, c->nsm * occ);
+            for (int tries = 0;; ++tries) {
+                // 3 flavours: blocks split in halves by particle class
+                const int per = c->nflav == 3 ? nb / 2 : nb;
+                int chunk = (c->ncell + per - 1) / per;
+                chunk = std::max(32, (chunk + 31) / 32 * 32);
+                c->nblocks = c->nflav == 3 ? 2 * per : nb;
+                c->chunk = chunk;
+                c->ntr_max = chunk / c->E + 2;
+                size_t smax = 0;
+                if (c->nflav == 3) {
+                    smax = stage3_smem_bytes(c->ntr_max);
+                } else {
+                    for (int st : {0, 2, 3, 4})
+                        for (int sch : {0, 1}) smax = std::max(smax, stage_smem_bytes(st, sch, c->ntr_max));
+                }
+                if (smax > 200 * 1024)
+                    throw Error(OSC_ERR_CONFIG, "osc_create: trajectory records exceed shared memory");
+                for (int st : {0, 2, 3, 4})
+                    CUDA_OK(cudaFuncSetAttribute(stage_kernel(c->nflav, desc->model, st),
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smax));
+                if (c->nflav == 3 || tries >= 3 || chunk <= 32 * 32) break;
+                int per_sm = 0;
+                CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, stage_kernel(2, desc->model, 4),
+                                                                      kBlock, smax));
+                if (per_sm >= occ) break;
+                nb *= 2;
+            }
             // magic numbers for the division by E inside the kernels
             uint32_t l = 0;
             while ((1u << l) < (uint32_t)c->E) ++l;
