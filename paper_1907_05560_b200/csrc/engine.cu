@@ -89,12 +89,12 @@ void check(int rc, const char* what) {
 using StageFn = void (*)(StepArgs);
 
 template <int MODEL>
-StageFn stage_fn(int stage) {
+StageFn stage_fn(int stage, int schedule) {
     switch (stage) {
         case 0: return k_stage<MODEL, 0>;
         case 2: return k_stage<MODEL, 2>;
         case 3: return k_stage<MODEL, 3>;
-        default: return k_stage<MODEL, 4>;
+        default: return schedule == 1 ? k_stage<MODEL, 4, 1> : k_stage<MODEL, 4, 0>;
     }
 }
 template <int MODEL>
@@ -117,14 +117,14 @@ PersistFn persist_kernel(int model) {
     }
 }
 
-StageFn stage_kernel(int nflav, int model, int stage) {
+StageFn stage_kernel(int nflav, int model, int stage, int schedule = 1) {
     if (nflav == 3) return model == 0 ? stage3_fn<0>(stage) : stage3_fn<1>(stage);
     switch (model) {
-        case 0: return stage_fn<0>(stage);
-        case 1: return stage_fn<1>(stage);
-        case 2: return stage_fn<2>(stage);
-        case 3: return stage_fn<3>(stage);
-        default: return stage_fn<4>(stage);
+        case 0: return stage_fn<0>(stage, schedule);
+        case 1: return stage_fn<1>(stage, schedule);
+        case 2: return stage_fn<2>(stage, schedule);
+        case 3: return stage_fn<3>(stage, schedule);
+        default: return stage_fn<4>(stage, schedule);
     }
 }
 
@@ -200,11 +200,11 @@ struct OscCtx {
     // one is scheduled while its predecessor drains (griddepcontrol in the
     // kernels orders the dependent reads).
     void launch_stage(int stage) {
-        const StageFn fn = stage_kernel(nflav, desc.model, stage);
+        const StageFn fn = stage_kernel(nflav, desc.model, stage, schedule);
         cudaLaunchConfig_t cfg{};
         cfg.gridDim = dim3(nblocks);
         cfg.blockDim = dim3(kBlock);
-        cfg.dynamicSmemBytes = nflav == 3 ? stage3_smem_bytes(ntr_max) : stage_smem_bytes(stage, schedule, ntr_max);
+        cfg.dynamicSmemBytes = nflav == 3 ? stage3_smem_bytes(ntr_max) : stage_smem_bytes(stage, schedule, ntr_max, E);
         cfg.stream = stream;
         cudaLaunchAttribute attr[1];
         attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -263,7 +263,7 @@ struct OscCtx {
 
     size_t persist_smem() const {
         size_t m = 0;
-        for (int st : {2, 3, 4}) m = std::max(m, stage_smem_bytes(st, schedule, ntr_max));
+        for (int st : {2, 3, 4}) m = std::max(m, stage_smem_bytes(st, schedule, ntr_max, E));
         return m;
     }
 
@@ -285,7 +285,7 @@ struct OscCtx {
     }
 
     void enqueue_steps(int n) {
-        if (persist && n > 1) {
+        if (persist && n > 1 && schedule == 1) {  // (the persistent kernel reads the stash)
             launch_persist(n);
             return;
         }
@@ -508,16 +508,17 @@ int osc_create(const OscDesc* desc, const OscComm* comm, OscCtx** out) {
                     smax = stage3_smem_bytes(c->ntr_max);
                 } else {
                     for (int st : {0, 2, 3, 4})
-                        for (int sch : {0, 1}) smax = std::max(smax, stage_smem_bytes(st, sch, c->ntr_max));
+                        for (int sch : {0, 1}) smax = std::max(smax, stage_smem_bytes(st, sch, c->ntr_max, c->E));
                 }
                 if (smax > 200 * 1024)
                     throw Error(OSC_ERR_CONFIG, "osc_create: trajectory records exceed shared memory");
                 for (int st : {0, 2, 3, 4})
-                    CUDA_OK(cudaFuncSetAttribute(stage_kernel(c->nflav, desc->model, st),
-                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smax));
+                    for (int sch : {0, 1})
+                        CUDA_OK(cudaFuncSetAttribute(stage_kernel(c->nflav, desc->model, st, sch),
+                                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smax));
                 if (c->nflav == 3 || tries >= 3 || chunk <= 32 * 32) break;
                 int per_sm = 0;
-                CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, stage_kernel(2, desc->model, 4),
+                CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, stage_kernel(2, desc->model, 4, 1),
                                                                       kBlock, smax));
                 if (per_sm >= occ) break;
                 nb *= 2;
@@ -562,6 +563,7 @@ int osc_create(const OscDesc* desc, const OscComm* comm, OscCtx** out) {
         a.ncell = c->ncell;
         a.npad = c->npad;
         a.chunk = c->chunk;
+        a.ntr_max = c->ntr_max;
         a.nranks = c->nranks;
         a.fuse_ctl = c->nranks == 1;
         a.e_magic = c->e_magic;
