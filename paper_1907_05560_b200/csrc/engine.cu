@@ -493,7 +493,7 @@ int osc_create(const OscDesc* desc, const OscComm* comm, OscCtx** out) {
         // per trajectory: the cylinder model), the grid doubles (two waves of
         // half-size chunks) instead of running at half occupancy.
         {
-            const int occ = OSC_MIN_BLOCKS;
+            const int occ = desc->nflav == 3 ? OSC3_MIN_BLOCKS : OSC_MIN_BLOCKS;
             int nb = std::max(1, c->nsm * occ);
             for (int tries = 0;; ++tries) {
                 // 3 flavours: blocks split in halves by particle class

@@ -20,6 +20,10 @@ namespace oscb200 {
 
 constexpr int kNM3Max = 18;  // 9 x (a, b): single-angle and bulb geometries
 
+#ifndef OSC3_MIN_BLOCKS
+#define OSC3_MIN_BLOCKS 1  // resident 3-flavour blocks per SM the register budget targets
+#endif
+
 struct TrajRec3 {
     double hb[4][9];   // beam part (H_nunu + matter) for H0..H3, particle convention
     double dl[3];
@@ -83,7 +87,7 @@ __device__ __forceinline__ void weighted_rho3(const double (&y)[3][6], const dou
 }
 
 template <int MODEL, int STAGE>
-__global__ void __launch_bounds__(kBlock, 1) k_stage3(StepArgs a) {
+__global__ void __launch_bounds__(kBlock, OSC3_MIN_BLOCKS) k_stage3(StepArgs a) {
     using Tr = StageTraits<STAGE>;
     constexpr int NG = MODEL == 0 ? 1 : 2;  // geometric moments (a | a, b)
     constexpr int NM = 9 * NG;
