@@ -121,6 +121,28 @@ typedef struct OscHookInfo {
  * retain the pointer. */
 typedef void (*osc_hook_fn)(void* user, const OscHookInfo* info, const double* state, size_t n);
 
+/* io::DumpGates (snapshot.hpp:134-138): a dump is due after an accepted step
+ * once r, wall time or iterations moved by the step since the last dump of
+ * that mode (io::should_dump, snapshot.cpp:237-243); 0 disables a gate. */
+typedef struct OscDumpGates {
+    double r_step, t_step;
+    uint64_t itr_step;
+} OscDumpGates;
+
+/* io::RecordMeta (snapshot.hpp:40-45) of a dump. */
+typedef struct OscRecordMeta {
+    uint64_t iter;
+    double r, dr, t_wall;
+} OscRecordMeta;
+
+/* Snapshot callback: mode 1 = whole local state (mode-1 payload layout,
+ * solver::extract_mode1 solver.cpp:127-140), mode 2 = energy-averaged
+ * |psi_e|^2 per (trajectory, species) (solver::extract_mode2
+ * solver.cpp:160-174).  Delivered in dump order on the calling thread; the
+ * payload lives in pinned host memory owned by the engine and is valid only
+ * during the call. */
+typedef void (*osc_dump_fn)(void* user, int mode, const OscRecordMeta* meta, const double* payload, size_t n);
+
 typedef struct OscCtx OscCtx;
 
 const char* osc_last_error(void);
@@ -155,6 +177,21 @@ int osc_trial_step_error(OscCtx* ctx, double r, double dr, double* err);
  * eps0 is huge).  hook may be NULL. */
 int osc_run(OscCtx* ctx, const OscStepControl* ctl, osc_hook_fn hook, void* user,
             OscRunSummary* out);
+
+/* Engine::run with the CLI's dump gating (DumpDriver, tools/oscflat.cpp:
+ * 46-118) moved next to the device: gates[0] for mode 1, gates[1] for mode 2,
+ * mode_mask bit 0/1 enables them.  Radius and iteration gates are evaluated
+ * by the device control update after every accepted step, which pauses the
+ * step sequence only when a dump is due; the state is packed on the device
+ * and copied to pinned host memory on a separate stream while the next steps
+ * run (async device-to-host snapshot I/O), and the callback fires when the
+ * copy has landed.  Wall-time gates are evaluated at batch boundaries. */
+int osc_run_dumps(OscCtx* ctx, const OscStepControl* ctl, const OscDumpGates* gates, int mode_mask,
+                  osc_dump_fn fn, void* user, OscRunSummary* out);
+
+/* solver::extract_mode2 (solver.cpp:160-174) on the device: n = local
+ * trajectories x species doubles (species: 4 for 2 flavours, 6 for 3). */
+int osc_extract_mode2(OscCtx* ctx, double* out, size_t n);
 
 /* max over local beams of |norm - 1| (beam.cpp:147-155). */
 int osc_max_norm_dev(OscCtx* ctx, double* out);

@@ -47,6 +47,10 @@ def host_isa() -> str:
 
 
 # --------------------------------------------------------------------------- ref
+_REF_DUMP_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_int, C.c_uint64, C.c_double, C.c_double,
+                           C.POINTER(C.c_double), C.c_size_t)
+
+
 class Ref:
     """Reference engine (solver::Engine) over a config text."""
 
@@ -74,6 +78,8 @@ class Ref:
         L.ref_e_sum.argtypes = [C.c_int, _dp, _dp, _dp]
         L.ref_partial_hvv.argtypes = [C.c_char_p, C.c_double, _dp, _dp, _dp]
         L.ref_fill_cache.argtypes = [C.c_char_p, C.c_double, _dp]
+        L.ref_run_dumps.argtypes = [C.c_char_p, C.c_int, _dp, _dp, C.c_int, _REF_DUMP_FN, C.c_void_p, _dp]
+        L.ref_extract_mode2.argtypes = [C.c_char_p, _dp, _dp]
 
     def _check(self, rc):
         if rc != 0:
@@ -109,6 +115,29 @@ class Ref:
         keys = ("final_r", "iterations", "accepted", "rejected", "wall_s", "final_max_norm_dev",
                 "phase_evolve_s")
         return out, dict(zip(keys, summ.tolist()))
+
+    def run_dumps(self, cfg_text: str, gates, mode_mask: int, lanes: int = 1, state=None):
+        """Engine::run + the CLI's DumpDriver gating; returns ([(mode, iter, r,
+        dr, payload)], final mode-1 state)."""
+        g = np.ascontiguousarray(np.asarray(gates, dtype=np.float64).ravel())
+        dumps = []
+
+        def _cb(user, mode, it, r, dr, payload, n):
+            dumps.append((int(mode), int(it), r, dr, np.ctypeslib.as_array(payload, shape=(n,)).copy()))
+
+        cb = _REF_DUMP_FN(_cb)
+        out = np.zeros(self.state_size(cfg_text))
+        sin = None if state is None else np.ascontiguousarray(state, dtype=np.float64)
+        self._check(self.lib.ref_run_dumps(cfg_text.encode(), lanes, None if sin is None else _ptr(sin),
+                                           _ptr(g), mode_mask, cb, None, _ptr(out)))
+        return dumps, out
+
+    def extract_mode2(self, cfg_text: str, state):
+        d = self.dims(cfg_text)
+        out = np.zeros(d["abins"] * d["pbins"] * 4)
+        sin = np.ascontiguousarray(state, dtype=np.float64)
+        self._check(self.lib.ref_extract_mode2(cfg_text.encode(), _ptr(sin), _ptr(out)))
+        return out
 
     def trial_step(self, cfg_text: str, r: float, dr: float, state=None):
         n = self.state_size(cfg_text)

@@ -30,6 +30,7 @@
 #include "oscflat/config.hpp"
 #include "oscflat/geometry.hpp"
 #include "oscflat/matter.hpp"
+#include "oscflat/snapshot.hpp"
 #include "oscflat/solver.hpp"
 #include "oscflat/spectra.hpp"
 
@@ -165,6 +166,63 @@ int ref_run(const char* cfg_text, int lanes, const double* state_in, double r, d
             summary[5] = s.final_max_norm_dev;
             summary[6] = s.phase_evolve_s;
         }
+    });
+}
+
+/// Engine::run with the CLI's dump gating (tools/oscflat.cpp:46-118
+/// DumpDriver::on_step + io::should_dump): gates[m*3 + {0,1,2}] = r_step,
+/// t_step, itr_step of mode m+1; fn receives each due dump (mode 1:
+/// extract_mode1, mode 2: extract_mode2) in order.
+typedef void (*ref_dump_fn)(void* user, int mode, uint64_t iter, double r, double dr, const double* payload,
+                            size_t n);
+int ref_run_dumps(const char* cfg_text, int lanes, const double* state_in, const double* gates, int mode_mask,
+                  ref_dump_fn fn, void* user, double* state_out) {
+    return guard([&] {
+        const auto cfg = cfg_of(cfg_text);
+        const auto env = solver::Environment::from_config(cfg);
+        solver::Engine engine(env, lanes);
+        engine.init_states();
+        const std::size_t n = static_cast<std::size_t>(env.grid.trajectories()) * 4 * 4 * env.ebins;
+        if (state_in) solver::fill_mode1(engine.state(), env.grid, {state_in, n});
+        const auto ctl = solver::StepControl::from_config(cfg);
+        io::DumpGates g[2];
+        io::DumpMarks marks[2];
+        for (int m = 0; m < 2; ++m) {
+            g[m] = {gates[m * 3], gates[m * 3 + 1], static_cast<std::uint64_t>(gates[m * 3 + 2])};
+            marks[m] = {ctl.r, 0.0, ctl.iter};
+        }
+        std::vector<double> payload;
+        engine.run(ctl, [&](const solver::HookInfo& info, const solver::BeamSet& set) {
+            for (int m = 0; m < 2; ++m) {
+                if (!(mode_mask >> m & 1)) continue;
+                if (!io::should_dump(g[m], info.r, info.t_wall, info.iter, marks[m])) continue;
+                if (m == 0)
+                    solver::extract_mode1(set, env.grid, payload);
+                else
+                    solver::extract_mode2(set, env.grid, env, payload);
+                fn(user, m + 1, info.iter, info.r, info.dr, payload.data(), payload.size());
+                marks[m] = {info.r, info.t_wall, info.iter};
+            }
+        });
+        if (state_out) {
+            solver::extract_mode1(engine.state(), env.grid, payload);
+            std::memcpy(state_out, payload.data(), payload.size() * sizeof(double));
+        }
+    });
+}
+
+/// solver::extract_mode2 of a mode-1 payload.
+int ref_extract_mode2(const char* cfg_text, const double* state_in, double* out) {
+    return guard([&] {
+        const auto cfg = cfg_of(cfg_text);
+        const auto env = solver::Environment::from_config(cfg);
+        solver::Engine engine(env, 1);
+        engine.init_states();
+        const std::size_t n = static_cast<std::size_t>(env.grid.trajectories()) * 4 * 4 * env.ebins;
+        solver::fill_mode1(engine.state(), env.grid, {state_in, n});
+        std::vector<double> payload;
+        solver::extract_mode2(engine.state(), env.grid, env, payload);
+        std::memcpy(out, payload.data(), payload.size() * sizeof(double));
     });
 }
 

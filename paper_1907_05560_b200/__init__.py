@@ -7,9 +7,9 @@ reference's ``solver`` API used by the tests and the bench.
 """
 from .config import BASELINE_CONFIGS, RunConfig, baseline_config, parse_config  # noqa: F401
 from .engine import (ConfigError, Engine, Environment, HookInfo, IoError,  # noqa: F401
-                     NumericError, ParallelError, RunSummary, StepControl, comm_unique_id,
-                     fermi_integral)
+                     NumericError, ParallelError, RecordMeta, RunSummary, StepControl,
+                     comm_unique_id, fermi_integral, should_dump)
 
 __all__ = ["BASELINE_CONFIGS", "RunConfig", "baseline_config", "parse_config", "Engine",
-           "Environment", "StepControl", "RunSummary", "HookInfo", "ConfigError",
+           "Environment", "StepControl", "RunSummary", "HookInfo", "RecordMeta", "should_dump", "ConfigError",
            "NumericError", "IoError", "ParallelError", "comm_unique_id", "fermi_integral"]

@@ -176,6 +176,12 @@ struct OscCtx {
 
     DevBuf<double> cos2, sin0, cphi, sphi, vac11, vac12, g;
     DevBuf<double> psi[2], stash, xbuf, xsend, partials, staging;
+    // snapshot I/O: spectrum weights [nsp][E] (mode 2), mode-2 output, the
+    // second packing buffer and pinned host buffers of the async dumps
+    DevBuf<double> fw, mode2buf, staging2;
+    cudaStream_t copy_stream = nullptr;
+    double* pinned[2] = {nullptr, nullptr};
+    size_t pinned_n = 0;
     DevBuf<Ctl> ctl;
     DevBuf<unsigned long long> scratch;
     Ctl* h_ctl = nullptr;  // pinned mirror
@@ -193,6 +199,9 @@ struct OscCtx {
             }
         }
         if (h_ctl) cudaFreeHost(h_ctl);
+        for (double* p : pinned)
+            if (p) cudaFreeHost(p);
+        if (copy_stream) cudaStreamDestroy(copy_stream);
         if (stream) cudaStreamDestroy(stream);
     }
 
@@ -339,6 +348,8 @@ struct OscCtx {
         h.err = 0.0;
         h.status = h.reason = 0;
         h.bad_sums = 0;
+        h.dump_mask = 0;  // snapshot gates are armed by osc_run_dumps only
+        h.pause = 0;
         h.commit = commit;
         h.dr_max = c.dr_max;
         h.dr_min = c.dr_min;
@@ -467,6 +478,7 @@ int osc_create(const OscDesc* desc, const OscComm* comm, OscCtx** out) {
             for (int e = 0; e < c->E; ++e)
                 g[(size_t)s * c->E + e] = ((s & 1) ? -1.0 : 1.0) * cpl[s] * fw[(size_t)s * c->E + e];
         upload(c->g, g.data(), g.size());
+        upload(c->fw, fw, (size_t)nsp * c->E);
         if (c->nflav == 3) upload(c->vac3, desc->vac3, 9 * (size_t)c->E);
         const size_t plane = (size_t)c->npad * c->nplanes;
         c->psi[0].alloc(plane);
@@ -856,6 +868,194 @@ int osc_max_norm_dev(OscCtx* c, double* out) {
         double v;
         std::memcpy(&v, &bits, sizeof v);
         *out = v;
+    });
+}
+
+static size_t mode2_doubles(const OscCtx* c) { return (size_t)c->ntraj * (c->nflav == 3 ? 6 : 4); }
+
+// Enqueue the mode-2 extraction into mode2buf (context stream).
+static void enqueue_mode2(OscCtx* c) {
+    const size_t n = mode2_doubles(c);
+    if (c->mode2buf.n < n) c->mode2buf.alloc(n);
+    k_mode2<<<(int)std::min<size_t>((n + 255) / 256, (size_t)c->nsm * 8), 256, 0, c->stream>>>(c->args, c->fw.p,
+                                                                                             c->mode2buf.p);
+    c->count();
+    CUDA_OK(cudaGetLastError());
+}
+
+int osc_extract_mode2(OscCtx* c, double* out, size_t n) {
+    return guarded([&] {
+        if (n != mode2_doubles(c)) throw Error(OSC_ERR_IO, "extract_mode2: payload size mismatch");
+        CUDA_OK(cudaSetDevice(c->device));
+        enqueue_mode2(c);
+        CUDA_OK(cudaMemcpyAsync(out, c->mode2buf.p, n * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+        CUDA_OK(cudaStreamSynchronize(c->stream));
+    });
+}
+
+int osc_run_dumps(OscCtx* c, const OscStepControl* ctl, const OscDumpGates* gates, int mode_mask,
+                  osc_dump_fn fn, void* user, OscRunSummary* out) {
+    return guarded([&] {
+        using Clock = std::chrono::steady_clock;
+        if (!ctl || !out || (mode_mask && (!gates || !fn)))
+            throw Error(OSC_ERR_CONFIG, "osc_run_dumps: null argument");
+        mode_mask &= 3;
+        CUDA_OK(cudaSetDevice(c->device));
+        const auto t0 = Clock::now();
+        auto secs = [&] { return std::chrono::duration<double>(Clock::now() - t0).count(); };
+        c->begin(*ctl, 1);
+        // arm the device gates (DumpDriver::reset_marks: marks at the start)
+        {
+            c->download_ctl();
+            Ctl& h = *c->h_ctl;
+            h.dump_mask = mode_mask;
+            h.pause = 0;
+            for (int m = 0; m < 2; ++m) {
+                h.dump_r_step[m] = (mode_mask >> m & 1) ? gates[m].r_step : 0.0;
+                h.dump_itr_step[m] = (mode_mask >> m & 1) ? gates[m].itr_step : 0;
+                h.mark_r[m] = ctl->r;
+                h.mark_iter[m] = ctl->iter;
+            }
+            c->upload_ctl();
+        }
+        double mark_t[2] = {0.0, 0.0};
+        const size_t n1 = (size_t)c->ncell * c->nplanes, n2 = mode2_doubles(c);
+        if (mode_mask & 1) {
+            if (c->staging.n < n1) c->staging.alloc(n1);
+            if (c->staging2.n < n1) c->staging2.alloc(n1);
+        }
+        if (mode_mask & 2 && c->mode2buf.n < n2) c->mode2buf.alloc(n2);
+        const size_t pin_n = std::max((mode_mask & 1) ? n1 : 0, (mode_mask & 2) ? n2 : 0);
+        if (pin_n > c->pinned_n) {
+            for (double*& p : c->pinned) {
+                if (p) cudaFreeHost(p);
+                p = nullptr;
+                CUDA_OK(cudaMallocHost(&p, pin_n * sizeof(double)));
+            }
+            c->pinned_n = pin_n;
+        }
+        if (mode_mask && !c->copy_stream)
+            CUDA_OK(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+
+        // Two dump slots in flight: packed on the compute stream into a
+        // device staging buffer, copied to pinned memory on the copy stream
+        // while the next steps run; delivered in order.
+        struct Pending {
+            int mode = 0;
+            size_t n = 0;
+            OscRecordMeta meta{};
+            cudaEvent_t done = nullptr;
+            bool busy = false;
+        } slot[2];
+        std::vector<int> fifo;
+        double t_io = 0.0;
+        auto deliver = [&](bool wait_all, int need_free) {
+            while (!fifo.empty()) {
+                Pending& p = slot[fifo.front()];
+                if (!wait_all && need_free < 0) {
+                    if (cudaEventQuery(p.done) == cudaErrorNotReady) break;
+                }
+                CUDA_OK(cudaEventSynchronize(p.done));
+                const auto ti = Clock::now();
+                fn(user, p.mode, &p.meta, c->pinned[fifo.front()], p.n);
+                t_io += std::chrono::duration<double>(Clock::now() - ti).count();
+                p.busy = false;
+                const int freed = fifo.front();
+                fifo.erase(fifo.begin());
+                if (!wait_all && need_free >= 0 && freed == need_free) break;
+            }
+        };
+        auto take_dump = [&](int mode, const OscRecordMeta& meta) {
+            int k = !slot[0].busy ? 0 : (!slot[1].busy ? 1 : -1);
+            if (k < 0) {  // both in flight: deliver the oldest
+                deliver(false, fifo.front());
+                k = !slot[0].busy ? 0 : 1;
+            }
+            Pending& p = slot[k];
+            if (!p.done) CUDA_OK(cudaEventCreateWithFlags(&p.done, cudaEventDisableTiming));
+            const double* src;
+            if (mode == 1) {
+                double* st = k == 0 ? c->staging.p : c->staging2.p;
+                k_pack<<<c->nsm * 8, 256, 0, c->stream>>>(c->args, st, n1);
+                c->count();
+                CUDA_OK(cudaGetLastError());
+                src = st;
+                p.n = n1;
+            } else {
+                enqueue_mode2(c);
+                src = c->mode2buf.p;
+                p.n = n2;
+            }
+            CUDA_OK(cudaEventRecord(p.done, c->stream));
+            CUDA_OK(cudaStreamWaitEvent(c->copy_stream, p.done, 0));
+            CUDA_OK(cudaMemcpyAsync(c->pinned[k], src, p.n * sizeof(double), cudaMemcpyDeviceToHost,
+                                    c->copy_stream));
+            CUDA_OK(cudaEventRecord(p.done, c->copy_stream));
+            if (mode == 2) CUDA_OK(cudaStreamWaitEvent(c->stream, p.done, 0));  // mode2buf reuse
+            p.mode = mode;
+            p.meta = meta;
+            p.busy = true;
+            fifo.push_back(k);
+        };
+
+        int term = c->h_ctl->terminate;
+        uint64_t last_acc = 0;
+        auto next_batch = [&]() {
+            int batch = 64;
+            if (ctl->Ts > 0) {
+                const uint64_t left = ctl->Ts - std::min<uint64_t>(ctl->Ts, c->h_ctl->iter);
+                batch = (int)std::max<uint64_t>(1, std::min<uint64_t>(left, 64));
+            }
+            c->enqueue_steps(batch);
+        };
+        if (!term) next_batch();
+        while (!term) {
+            c->download_ctl();
+            c->raise_device_status();
+            Ctl& h = *c->h_ctl;
+            term = h.terminate;
+            int due = h.pause & mode_mask;
+            const double t = secs();
+            if (h.accepted != last_acc) {  // wall-time gates at batch boundaries
+                for (int m = 0; m < 2; ++m)
+                    if ((mode_mask >> m & 1) && gates[m].t_step > 0.0 && t - mark_t[m] >= gates[m].t_step)
+                        due |= 1 << m;
+                last_acc = h.accepted;
+            }
+            if (due) {
+                const OscRecordMeta meta{h.iter, h.r, h.dr, t};
+                for (int m = 0; m < 2; ++m) {
+                    if (!(due >> m & 1)) continue;
+                    mark_t[m] = t;
+                    h.mark_r[m] = h.r;  // (already moved by the device for its own gates)
+                    h.mark_iter[m] = h.iter;
+                    take_dump(m + 1, meta);
+                }
+                h.pause = 0;
+                CUDA_OK(cudaMemcpyAsync(c->ctl.p, c->h_ctl, sizeof(Ctl), cudaMemcpyHostToDevice, c->stream));
+            }
+            if (!term && ctl->Tn > 0.0 && secs() >= ctl->Tn) term = 3;
+            // keep the device busy while the host delivers finished dumps
+            if (!term) next_batch();
+            deliver(false, -1);
+        }
+        deliver(true, -1);
+        for (Pending& p : slot)
+            if (p.done) cudaEventDestroy(p.done);
+        double nd = 0.0;
+        osc_max_norm_dev(c, &nd);
+        const Ctl& h = *c->h_ctl;
+        out->final_r = h.r;
+        out->iterations = h.iter - ctl->iter;
+        out->accepted = h.accepted;
+        out->rejected = h.rejected;
+        out->wall_s = secs();
+        out->phase_hamiltonian_s = 0.0;
+        out->phase_evolve_s = out->wall_s - t_io;
+        out->phase_io_s = t_io;
+        out->max_worker_wait_s = 0.0;
+        out->final_max_norm_dev = nd;
+        out->termination = term == 2 ? 2 : (term == 3 ? 3 : 1);
     });
 }
 

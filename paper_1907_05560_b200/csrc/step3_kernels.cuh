@@ -99,7 +99,7 @@ __global__ void __launch_bounds__(kBlock, OSC3_MIN_BLOCKS) k_stage3(StepArgs a) 
 
     const Ctl* ctl = a.ctl;
     grid_dependency_wait();
-    if (STAGE != 0 && (ctl->terminate || ctl->status)) return;
+    if (STAGE != 0 && (ctl->terminate || ctl->status || ctl->pause)) return;
     const int tid = threadIdx.x;
     const int nb_half = gridDim.x / 2;
     const int pc = blockIdx.x >= nb_half;

@@ -21,8 +21,8 @@ import numpy as np
 
 from . import native
 from .config import RunConfig
-from .native import (HOOK_FN, OscComm, OscDesc, OscParams, OscRunSummary, OscStepControl, check,
-                     lib)
+from .native import (DUMP_FN, HOOK_FN, OscComm, OscDesc, OscDumpGates, OscParams, OscRunSummary,
+                     OscStepControl, check, lib)
 
 
 @dataclass
@@ -73,6 +73,26 @@ class RunSummary:
 
 @dataclass
 class HookInfo:
+    iter: int
+    r: float
+    dr: float
+    t_wall: float
+
+
+def should_dump(gates, r: float, t_wall: float, it: int, last) -> bool:
+    """io::should_dump (snapshot.cpp:237-243): gates = (r_step, t_step,
+    itr_step), last = (r, t, iter) of the previous dump of that mode."""
+    r_step, t_step, itr_step = gates
+    if r_step > 0.0 and r - last[0] >= r_step:
+        return True
+    if t_step > 0.0 and t_wall - last[1] >= t_step:
+        return True
+    return itr_step > 0 and it - last[2] >= itr_step
+
+
+@dataclass
+class RecordMeta:
+    """io::RecordMeta (snapshot.hpp:40-45) of a dump."""
     iter: int
     r: float
     dr: float
@@ -221,6 +241,37 @@ class Engine:
                           s.phase_hamiltonian_s, s.phase_evolve_s, s.phase_io_s,
                           s.max_worker_wait_s, s.final_max_norm_dev,
                           _TERM.get(s.termination, "radius"))
+
+    def run_dumps(self, ctl: StepControl, gates, mode_mask: int, callback, copy: bool = True) -> RunSummary:
+        """Engine.run with the CLI's snapshot gating on the device
+        (tools/oscflat.cpp:46-118 DumpDriver): gates = [(r_step, t_step,
+        itr_step) for mode 1, same for mode 2]; callback(mode, RecordMeta,
+        payload) receives copies (copy=False: a view of the engine's pinned
+        buffer, valid only during the call), in dump order.  Mode-1 payloads are the
+        local state (extract_mode1 layout), mode-2 payloads
+        trajectories x species energy averages (extract_mode2)."""
+        g = (OscDumpGates * 2)(*[OscDumpGates(float(a), float(b), int(c)) for a, b, c in gates])
+
+        def _tramp(user, mode, meta, payload, n):
+            m = meta.contents
+            v = np.ctypeslib.as_array(payload, shape=(n,))
+            callback(int(mode), RecordMeta(m.iter, m.r, m.dr, m.t_wall), v.copy() if copy else v)
+
+        cb = DUMP_FN(_tramp)
+        s = OscRunSummary()
+        check(lib().osc_run_dumps(self._ctx, C.byref(ctl.to_c()), g, int(mode_mask), cb, None, C.byref(s)))
+        return RunSummary(s.final_r, s.iterations, s.accepted, s.rejected, s.wall_s,
+                          s.phase_hamiltonian_s, s.phase_evolve_s, s.phase_io_s,
+                          s.max_worker_wait_s, s.final_max_norm_dev,
+                          _TERM.get(s.termination, "radius"))
+
+    def mode2(self) -> np.ndarray:
+        """solver::extract_mode2 of the current state, computed on the device:
+        [trajectory][species] energy-averaged |psi_e|^2 (solver.cpp:160-174)."""
+        nsp = 6 if self.env.nflav == 3 else 4
+        out = np.zeros(self.state_doubles // (nsp * (6 if nsp == 6 else 4) * self.env.ebins) * nsp)
+        check(lib().osc_extract_mode2(self._ctx, out.ctypes.data_as(C.POINTER(C.c_double)), out.size))
+        return out
 
     # -- device-resident helpers (bench / tests) -------------------------
     def max_norm_dev(self) -> float:

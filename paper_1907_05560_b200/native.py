@@ -52,6 +52,17 @@ class OscHookInfo(C.Structure):
 HOOK_FN = C.CFUNCTYPE(None, C.c_void_p, C.POINTER(OscHookInfo), _dp, C.c_size_t)
 
 
+class OscDumpGates(C.Structure):
+    _fields_ = [("r_step", C.c_double), ("t_step", C.c_double), ("itr_step", C.c_uint64)]
+
+
+class OscRecordMeta(C.Structure):
+    _fields_ = [("iter", C.c_uint64), ("r", C.c_double), ("dr", C.c_double), ("t_wall", C.c_double)]
+
+
+DUMP_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_int, C.POINTER(OscRecordMeta), _dp, C.c_size_t)
+
+
 class OscParams(C.Structure):
     _fields_ = [("model", C.c_int), ("abins", C.c_int), ("pbins", C.c_int), ("ebins", C.c_int),
                 ("Rnu", C.c_double), ("E0", C.c_double), ("E1", C.c_double),
@@ -70,7 +81,7 @@ class OscParams(C.Structure):
 SYMBOLS = [
     "osc_last_error", "osc_version", "osc_comm_unique_id", "osc_create", "osc_destroy",
     "osc_local_range", "osc_init_states", "osc_set_state", "osc_get_state",
-    "osc_set_state_device", "osc_get_state_device", "osc_trial_step_error", "osc_run",
+    "osc_set_state_device", "osc_get_state_device", "osc_trial_step_error", "osc_run", "osc_run_dumps", "osc_extract_mode2",
     "osc_max_norm_dev", "osc_begin", "osc_enqueue_steps", "osc_query", "osc_synchronize",
     "osc_stream", "osc_launches_per_step", "osc_debug_sums", "osc_set_schedule", "osc_set_persistent", "osc_get_persistent", "osc_launch_count",
     "osc_fp64_peak", "osc_profile_stages", "osc_env_build", "osc_env_desc", "osc_env_destroy", "osc_fermi_integral",
@@ -100,6 +111,9 @@ def lib() -> C.CDLL:
         getattr(L, f).argtypes = [vp, vp, C.c_size_t]
     L.osc_trial_step_error.argtypes = [vp, C.c_double, C.c_double, _dp]
     L.osc_run.argtypes = [vp, C.POINTER(OscStepControl), HOOK_FN, vp, C.POINTER(OscRunSummary)]
+    L.osc_run_dumps.argtypes = [vp, C.POINTER(OscStepControl), C.POINTER(OscDumpGates), C.c_int, DUMP_FN, vp,
+                                C.POINTER(OscRunSummary)]
+    L.osc_extract_mode2.argtypes = [vp, _dp, C.c_size_t]
     L.osc_max_norm_dev.argtypes = [vp, _dp]
     L.osc_begin.argtypes = [vp, C.POINTER(OscStepControl)]
     L.osc_enqueue_steps.argtypes = [vp, C.c_int]

@@ -14,7 +14,7 @@ import os
 import numpy as np
 import pytest
 
-from paper_1907_05560_b200 import (ConfigError, Engine, Environment, NumericError, StepControl,
+from paper_1907_05560_b200 import (ConfigError, Engine, Environment, NumericError, StepControl, should_dump,
                                    baseline_config, parse_config)
 
 pytestmark = pytest.mark.gpu
@@ -440,3 +440,77 @@ def test_persistent_kernel_bit_identical_to_stage_kernels(model):
     assert ia == 40 and ra > 0
     assert np.array_equal(sa_, sb)
     assert la < lb  # one launch per batch instead of three per step
+
+
+# ---- snapshot I/O: device-gated dumps with async D2H ----
+DUMP_CFG = dict(Abins=8, Ebins=10, R0=50, Rn=50.2, dr=0.001, max_dr=0.05, eps0=1e-8)
+
+
+def test_dumps_follow_reference_gating(ref):
+    """Same dump sequence (mode, iteration, r, dr) and payloads as the
+    reference engine driven by the CLI's DumpDriver gating
+    (tools/oscflat.cpp:46-118, io::should_dump snapshot.cpp:237-243)."""
+    cfg = baseline_config("configs0", **DUMP_CFG)
+    gates = [(0.0, 0.0, 8), (0.02, 0.0, 0)]
+    want, want_final = ref.run_dumps(cfg.render(), gates, 3)
+    env, eng = make(cfg)
+    got = []
+    s = eng.run_dumps(StepControl.from_config(cfg), gates, 3, lambda m, meta, p: got.append((m, meta, p)))
+    assert len(want) > 20 and any(m == 2 for m, *_ in want)
+    assert [(m, it) for m, it, *_ in want] == [(m, meta.iter) for m, meta, _ in got]
+    for (m, it, r, dr, pw), (_, meta, pg) in zip(want, got):
+        assert meta.r == pytest.approx(r, rel=1e-13) and meta.dr == pytest.approx(dr, rel=1e-9)
+        if m == 1:
+            (rg, _), (rw, _) = density(pg, env.ebins), density(pw, env.ebins)
+            assert np.max(np.abs(rg - rw)) <= RHO_TOL
+        else:
+            assert pg.shape == pw.shape and np.max(np.abs(pg - pw)) <= 1e-12 * np.max(np.abs(pw))
+    assert s.iterations > 0 and np.max(np.abs(eng.state() - want_final)) <= 1e-8
+
+
+def test_dumps_equal_hook_states_bit_exact():
+    """The async device dumps deliver exactly the states a per-step hook sees
+    at the same accepted steps."""
+    cfg = baseline_config("configs0", **DUMP_CFG)
+    gates = [(0.0, 0.0, 5), (0.0, 0.0, 0)]
+    env, eng = make(cfg)
+    hooked, mark = [], (cfg.values["R0"], 0.0, 0)
+
+    def hook(info, state):
+        nonlocal mark
+        if should_dump(gates[0], info.r, 0.0, info.iter, mark):
+            hooked.append((info.iter, info.r, info.dr, state))
+            mark = (info.r, 0.0, info.iter)
+
+    eng.run(StepControl.from_config(cfg), hook)
+    env2, eng2 = make(cfg)
+    got = []
+    eng2.run_dumps(StepControl.from_config(cfg), gates, 1, lambda m, meta, p: got.append((meta, p)))
+    assert len(got) == len(hooked) > 10
+    for (it, r, dr, st), (meta, p) in zip(hooked, got):
+        assert (meta.iter, meta.r, meta.dr) == (it, r, dr)
+        assert np.array_equal(p, st)
+    # gates are disarmed afterwards: a plain run on the same engine finishes
+    s = eng2.run(StepControl.from_config(cfg))
+    assert s.termination in ("radius", "iterations") and s.iterations > 0
+
+
+def test_mode2_matches_reference_extract_mode2(ref):
+    cfg = baseline_config("configs0", Abins=16, Ebins=24, R0=50, Rn=50.01, dr=1e-4, max_dr=1e-4)
+    env, eng = make(cfg)
+    eng.run(StepControl.from_config(cfg))
+    want = ref.extract_mode2(cfg.render(), eng.state())
+    got = eng.mode2()
+    assert got.shape == want.shape
+    assert np.max(np.abs(got - want)) <= 1e-14 * np.max(np.abs(want))
+
+
+def test_mode2_three_flavour_is_electron_probability_average():
+    cfg = baseline_config("configs1", Abins=8, Ebins=6, R0=50, Rn=51, dr=1e-6, max_dr=1e-6, Ts=4)
+    env, eng = make(cfg)
+    eng.run(StepControl.from_config(cfg))
+    x = eng.state().reshape(-1, 6, 6, env.ebins)
+    fw = env.tables()["fw6"]
+    got = eng.mode2().reshape(-1, 6)
+    want = np.einsum("tse,se->ts", x[:, :, 0] ** 2 + x[:, :, 1] ** 2, fw)
+    assert np.max(np.abs(got - want)) <= 1e-13 * np.max(np.abs(want))
