@@ -214,14 +214,17 @@ int osc_debug_sums(OscCtx* ctx, double* out60);
 /* Configure the stage schedule: 0 = recompute intermediates from psi0,
  * 1 = stash half2 in HBM between S3 and S4. */
 int osc_set_schedule(OscCtx* ctx, int schedule);
-/* on=1: multi-step batches on a single-GPU 2-flavour context run as ONE
- * persistent cooperative kernel (grid barriers instead of kernel boundaries;
- * opt-in, also via env OSC_PERSIST=1).  on=0 (default): per-stage kernels
- * with programmatic dependent launch in a CUDA graph of 8 steps.  Returns
- * OSC_ERR_CONFIG when the persistent kernel is unavailable for this context. */
-int osc_set_persistent(OscCtx* ctx, int on);
-/* 1 if multi-step batches currently use the persistent kernel. */
-int osc_get_persistent(OscCtx* ctx);
+/* How step batches launch (single-GPU 2-flavour contexts; multi-GPU and
+ * 3-flavour contexts always use 0):
+ *   0  stage kernels with programmatic dependent launch, CUDA graphs of 8 steps;
+ *   1  one persistent cooperative kernel streaming the state from HBM, grid
+ *      barriers between stages (opt-in; measured slower than 0);
+ *   2  one persistent cooperative kernel with the whole local state resident
+ *      in shared memory (default when it fits: small problems, configs[0]).
+ * Env OSC_LAUNCH=0/1/2 overrides the default.  OSC_ERR_CONFIG when the mode is
+ * unavailable for this context. */
+int osc_set_launch_mode(OscCtx* ctx, int mode);
+int osc_get_launch_mode(OscCtx* ctx);
 /* Number of kernels this context has launched so far (graph launches count
  * every kernel node) — the bench's gpu_launches evidence. */
 unsigned long long osc_launch_count(const OscCtx* ctx);

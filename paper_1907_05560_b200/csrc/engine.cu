@@ -20,6 +20,7 @@
 #include "oscflat_b200.h"
 #include "status.hpp"
 #include "step3_kernels.cuh"
+#include "resident_kernels.cuh"
 #include "step_kernels.cuh"
 
 namespace oscb200 {
@@ -117,6 +118,17 @@ PersistFn persist_kernel(int model) {
     }
 }
 
+using ResidentFn = void (*)(StepArgs, int, int, int, double*, unsigned*);
+ResidentFn resident_kernel(int model) {
+    switch (model) {
+        case 0: return k_resident<0>;
+        case 1: return k_resident<1>;
+        case 2: return k_resident<2>;
+        case 3: return k_resident<3>;
+        default: return k_resident<4>;
+    }
+}
+
 StageFn stage_kernel(int nflav, int model, int stage, int schedule = 1) {
     if (nflav == 3) return model == 0 ? stage3_fn<0>(stage) : stage3_fn<1>(stage);
     switch (model) {
@@ -162,8 +174,13 @@ struct OscCtx {
     int nplanes = 16;  // state planes per buffer
     DevBuf<double> vac3;
     int use_pdl = 1;
-    int persist_ok = 0;  // the persistent kernel fits one resident wave
-    int persist = 0;     // multi-step batches use the persistent kernel
+    int persist_ok = 0;   // the persistent streaming kernel fits one resident wave
+    int resident_ok = 0;  // the whole state fits in shared memory (k_resident)
+    int launch_mode = 0;  // 0 stage kernels + graphs, 1 persistent streaming, 2 resident
+    int rch = 0, rntr = 0;
+    size_t rsmem = 0;
+    DevBuf<double> rpart;
+    DevBuf<unsigned> rbar;
     unsigned long long nlaunch = 0;  // kernels this context launched
     bool capturing = false;
     int graph_kernels = 0;
@@ -293,8 +310,31 @@ struct OscCtx {
         count();
     }
 
+    // n steps in one cooperative launch with the state resident in shared
+    // memory (single GPU, small problems).
+    void launch_resident(int n) {
+        CUDA_OK(cudaMemsetAsync(rbar.p, 0, sizeof(unsigned), stream));
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(nsm);
+        cfg.blockDim = dim3(kBlock);
+        cfg.dynamicSmemBytes = rsmem;
+        cfg.stream = stream;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeCooperative;
+        attr[0].val.cooperative = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        CUDA_OK(cudaLaunchKernelEx(&cfg, resident_kernel(desc.model), args, n, rch, rntr, rpart.p, rbar.p));
+        count();
+    }
+
     void enqueue_steps(int n) {
-        if (persist && n > 1 && schedule == 1) {  // (the persistent kernel reads the stash)
+        if (n <= 0) return;
+        if (launch_mode == 2) {
+            launch_resident(n);
+            return;
+        }
+        if (launch_mode == 1 && n > 1 && schedule == 1) {  // (the persistent kernel reads the stash)
             launch_persist(n);
             return;
         }
@@ -543,7 +583,7 @@ int osc_create(const OscDesc* desc, const OscComm* comm, OscCtx** out) {
         }
         c->partials.alloc((size_t)c->nblocks * kSlotDoubles);
 
-        // persistent kernel: single GPU, 2 flavours, one resident wave
+        // persistent kernels: single GPU, 2 flavours
         if (c->nranks == 1 && c->nflav == 2) {
             const PersistFn pf = persist_kernel(desc->model);
             const size_t sm = c->persist_smem();
@@ -551,10 +591,30 @@ int osc_create(const OscDesc* desc, const OscComm* comm, OscCtx** out) {
             int per_sm = 0;
             CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pf, kBlock, sm));
             c->persist_ok = (long)per_sm * c->nsm >= c->nblocks && OSC_DEBUG_MODE == 0;
-            // opt-in (OSC_PERSIST=1 or osc_set_persistent): measured slower
-            // than the PDL-pipelined stage kernels on every BASELINE config
-            const char* env = std::getenv("OSC_PERSIST");
-            c->persist = c->persist_ok && env && env[0] == '1';
+            // resident: the local state, the result and the stash of a chunk
+            // per SM in shared memory
+            c->rch = (c->ncell + c->nsm - 1) / c->nsm;
+            c->rntr = c->rch / c->E + 2;
+            c->rsmem = resident_smem_bytes(c->rch, c->rntr, c->E);
+            if (c->rsmem <= 200 * 1024 && OSC_DEBUG_MODE == 0) {
+                const ResidentFn rf = resident_kernel(desc->model);
+                CUDA_OK(cudaFuncSetAttribute(rf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->rsmem));
+                int rper = 0;
+                CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&rper, rf, kBlock, c->rsmem));
+                if (rper >= 1) {
+                    c->resident_ok = 1;
+                    c->rpart.alloc((size_t)2 * c->nsm * kSlotDoubles);
+                    c->rbar.alloc(1);
+                }
+            }
+            // default: resident where the state fits, else the PDL-pipelined
+            // stage kernels (the persistent streaming kernel measured slower);
+            // env OSC_LAUNCH=0/1/2 overrides
+            c->launch_mode = c->resident_ok ? 2 : 0;
+            if (const char* env = std::getenv("OSC_LAUNCH")) {
+                const int m = std::atoi(env);
+                if (m == 0 || (m == 1 && c->persist_ok) || (m == 2 && c->resident_ok)) c->launch_mode = m;
+            }
         }
 
         if (c->nranks > 1) {
@@ -786,15 +846,18 @@ int osc_set_schedule(OscCtx* c, int schedule) {
     });
 }
 
-int osc_set_persistent(OscCtx* c, int on) {
+int osc_set_launch_mode(OscCtx* c, int mode) {
     return guarded([&] {
-        if (on && !c->persist_ok)
+        if (mode < 0 || mode > 2) throw Error(OSC_ERR_CONFIG, "launch mode must be 0, 1 or 2");
+        if (mode == 1 && !c->persist_ok)
             throw Error(OSC_ERR_CONFIG, "persistent kernel unavailable (multi-rank, 3 flavours or occupancy)");
-        c->persist = on ? 1 : 0;
+        if (mode == 2 && !c->resident_ok)
+            throw Error(OSC_ERR_CONFIG, "resident kernel unavailable (multi-rank, 3 flavours or state too large)");
+        c->launch_mode = mode;
     });
 }
 
-int osc_get_persistent(OscCtx* c) { return c ? c->persist : 0; }
+int osc_get_launch_mode(OscCtx* c) { return c ? c->launch_mode : 0; }
 
 unsigned long long osc_launch_count(const OscCtx* c) { return c ? c->nlaunch : 0; }
 
@@ -1075,7 +1138,7 @@ int osc_run(OscCtx* c, const OscStepControl* ctl, osc_hook_fn hook, void* user, 
         // state, else graph batches with a host check between batches
         while (!term) {
             if (hook) {
-                c->enqueue_step();
+                c->enqueue_steps(1);
             } else {
                 int batch = 64;
                 if (ctl->Ts > 0) {

@@ -328,14 +328,17 @@ class Engine:
     def set_schedule(self, schedule: int) -> None:
         check(lib().osc_set_schedule(self._ctx, schedule))
 
-    def set_persistent(self, on: bool) -> None:
-        """Multi-step batches as one persistent cooperative kernel (default
-        where available) or as per-stage kernels in a CUDA graph."""
-        check(lib().osc_set_persistent(self._ctx, 1 if on else 0))
+    LAUNCH_STAGES, LAUNCH_PERSISTENT, LAUNCH_RESIDENT = 0, 1, 2
+
+    def set_launch_mode(self, mode: int) -> None:
+        """0: stage kernels (PDL, CUDA graphs); 1: persistent streaming kernel;
+        2: persistent kernel with the state resident in shared memory (the
+        default where it fits).  Raises ConfigError if unavailable."""
+        check(lib().osc_set_launch_mode(self._ctx, int(mode)))
 
     @property
-    def persistent(self) -> bool:
-        return bool(lib().osc_get_persistent(self._ctx))
+    def launch_mode(self) -> int:
+        return int(lib().osc_get_launch_mode(self._ctx))
 
     def launch_count(self) -> int:
         """Kernels this engine has launched so far (graph nodes included)."""

@@ -83,7 +83,7 @@ SYMBOLS = [
     "osc_local_range", "osc_init_states", "osc_set_state", "osc_get_state",
     "osc_set_state_device", "osc_get_state_device", "osc_trial_step_error", "osc_run", "osc_run_dumps", "osc_extract_mode2",
     "osc_max_norm_dev", "osc_begin", "osc_enqueue_steps", "osc_query", "osc_synchronize",
-    "osc_stream", "osc_launches_per_step", "osc_debug_sums", "osc_set_schedule", "osc_set_persistent", "osc_get_persistent", "osc_launch_count",
+    "osc_stream", "osc_launches_per_step", "osc_debug_sums", "osc_set_schedule", "osc_set_launch_mode", "osc_get_launch_mode", "osc_launch_count",
     "osc_fp64_peak", "osc_profile_stages", "osc_env_build", "osc_env_desc", "osc_env_destroy", "osc_fermi_integral",
 ]
 
@@ -125,8 +125,8 @@ def lib() -> C.CDLL:
     L.osc_launches_per_step.argtypes = [vp]
     L.osc_debug_sums.argtypes = [vp, _dp]
     L.osc_set_schedule.argtypes = [vp, C.c_int]
-    L.osc_set_persistent.argtypes = [vp, C.c_int]
-    L.osc_get_persistent.argtypes = [vp]
+    L.osc_set_launch_mode.argtypes = [vp, C.c_int]
+    L.osc_get_launch_mode.argtypes = [vp]
     L.osc_launch_count.argtypes = [vp]
     L.osc_launch_count.restype = C.c_ulonglong
     L.osc_fp64_peak.argtypes = [C.c_int, _dp, _dp]

@@ -429,7 +429,7 @@ def test_persistent_kernel_bit_identical_to_stage_kernels(model):
     for on in (True, False):
         env, eng = make(cfg)
         try:
-            eng.set_persistent(on)
+            eng.set_launch_mode(Engine.LAUNCH_PERSISTENT if on else Engine.LAUNCH_STAGES)
         except ConfigError:
             pytest.skip("persistent kernel unavailable on this device")
         n0 = eng.launch_count()

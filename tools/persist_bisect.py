@@ -10,7 +10,7 @@ for kv in ("Lve=1e51", "Lvae=1e51", "Lvt=1e51", "Lvat=1e51", "Abins=6", "R0=50",
     cfg.override(kv)
 
 def run(on, n):
-    env = Environment.from_config(cfg); eng = Engine(env); eng.init_states(); eng.set_persistent(on)
+    env = Environment.from_config(cfg); eng = Engine(env); eng.init_states(); eng.set_launch_mode(1 if on else 0)
     ctl = StepControl.from_config(cfg)
     eng.begin(ctl)
     eng.enqueue_steps(n); eng.synchronize()
