@@ -19,6 +19,7 @@
 //     to the global buffer Ctl::cur names.
 #pragma once
 
+#include "oscflat_b200.h"
 #include "step_kernels.cuh"
 
 namespace oscb200 {
@@ -58,11 +59,11 @@ __device__ __forceinline__ bool res_allreduce(double (&v)[NV], double mx, double
     const int tid = threadIdx.x;
     block_reduce<NV>(v, mx, S.red);
     double* slot = part + (size_t)(phase & 1) * gridDim.x * kSlotDoubles;
-    if (tid == 0) {
-        double* p = slot + (size_t)blockIdx.x * kSlotDoubles;
+    if (tid == 0) {  // [value][block] layout: the reads below coalesce
+        double* p = slot + blockIdx.x;
 #pragma unroll
-        for (int k = 0; k < NV; ++k) p[k] = v[k];
-        p[NV] = mx;
+        for (int k = 0; k < NV; ++k) p[(size_t)k * gridDim.x] = v[k];
+        p[(size_t)NV * gridDim.x] = mx;
         asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
         S.stop = res_wait(bar, (phase + 1) * gridDim.x) ? 0 : 1;
     }
@@ -74,10 +75,10 @@ __device__ __forceinline__ bool res_allreduce(double (&v)[NV], double mx, double
 #pragma unroll
     for (int k = 0; k < NV; ++k) fv[k] = 0.0;
     for (int b = tid; b < (int)gridDim.x; b += kBlock) {
-        const double* p = slot + (size_t)b * kSlotDoubles;
+        const double* p = slot + b;
 #pragma unroll
-        for (int k = 0; k < NV; ++k) fv[k] += __ldcg(p + k);
-        fm = fmax(fm, __ldcg(p + NV));
+        for (int k = 0; k < NV; ++k) fv[k] += __ldcg(p + (size_t)k * gridDim.x);
+        fm = fmax(fm, __ldcg(p + (size_t)NV * gridDim.x));
     }
     __syncthreads();  // S.red reuse
     block_reduce<NV>(fv, fm, S.red);

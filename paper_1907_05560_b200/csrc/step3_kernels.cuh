@@ -280,10 +280,12 @@ __global__ void __launch_bounds__(kBlock, OSC3_MIN_BLOCKS) k_stage3(StepArgs a) 
 
     block_reduce<NV>(acc, emax, red);
     if (tid == 0) {
-        double* p = a.partials + (size_t)blockIdx.x * kSlotDoubles;
+        // partials are stored [value][block]: the last block's loads of one
+        // value across blocks coalesce (one request per 32 blocks)
+        double* p = a.partials + blockIdx.x;
 #pragma unroll
-        for (int k = 0; k < NV; ++k) p[k] = acc[k];
-        p[NV] = emax;
+        for (int k = 0; k < NV; ++k) p[(size_t)k * gridDim.x] = acc[k];
+        p[(size_t)NV * gridDim.x] = emax;
         __threadfence();
         const unsigned ticket = atomicAdd(&a.ctl->counter[Tr::slot], 1u);
         is_last = ticket == gridDim.x - 1;
@@ -296,10 +298,10 @@ __global__ void __launch_bounds__(kBlock, OSC3_MIN_BLOCKS) k_stage3(StepArgs a) 
 #pragma unroll
     for (int k = 0; k < NV; ++k) fv[k] = 0.0;
     for (int b = tid; b < (int)gridDim.x; b += kBlock) {
-        const double* p = a.partials + (size_t)b * kSlotDoubles;
+        const double* p = a.partials + b;
 #pragma unroll
-        for (int k = 0; k < NV; ++k) fv[k] += __ldcg(p + k);
-        fm = fmax(fm, __ldcg(p + NV));
+        for (int k = 0; k < NV; ++k) fv[k] += __ldcg(p + (size_t)k * gridDim.x);
+        fm = fmax(fm, __ldcg(p + (size_t)NV * gridDim.x));
     }
     __syncthreads();
     block_reduce<NV>(fv, fm, red);

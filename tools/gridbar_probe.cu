@@ -1,0 +1,100 @@
+// Grid all-reduce latency probe (resident kernel's stage boundary): one
+// block per SM, N all-reduces of NV doubles; variants of the arrival/wait.
+#include <cstdio>
+#include <cuda_runtime.h>
+#include "../paper_1907_05560_b200/csrc/resident_kernels.cuh"
+using namespace oscb200;
+
+template <int NV, int VAR>
+__global__ void __launch_bounds__(kBlock, 1) k_probe(int n, double* part, unsigned* bar, double* out) {
+    __shared__ ResShared S;
+    unsigned phase = 0;
+    double acc = threadIdx.x * 1e-3;
+    for (int i = 0; i < n; ++i) {
+        double v[NV];
+#pragma unroll
+        for (int k = 0; k < NV; ++k) v[k] = acc + k;
+        if (VAR == 0) {
+            if (!res_allreduce<NV>(v, acc, part, bar, phase, S, S.fin)) break;
+        } else if (VAR == 2) {  // write partial + barrier, no read
+            block_reduce<NV>(v, acc, S.red);
+            double* slot = part + (size_t)(phase & 1) * gridDim.x * kSlotDoubles;
+            if (threadIdx.x == 0) {
+                double* p = slot + (size_t)blockIdx.x * kSlotDoubles;
+                for (int k = 0; k < NV; ++k) p[k] = v[k];
+                asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
+                res_wait(bar, (phase + 1) * gridDim.x);
+            }
+            ++phase;
+            __syncthreads();
+        } else if (VAR == 3) {  // barrier + read partials + reduce, no write
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
+                res_wait(bar, (phase + 1) * gridDim.x);
+            }
+            double* slot = part + (size_t)(phase & 1) * gridDim.x * kSlotDoubles;
+            ++phase;
+            __syncthreads();
+            double fv[NV];
+            double fm = 0.0;
+            for (int k = 0; k < NV; ++k) fv[k] = 0.0;
+            for (int b = threadIdx.x; b < (int)gridDim.x; b += kBlock) {
+                const double* p = slot + (size_t)b * kSlotDoubles;
+                for (int k = 0; k < NV; ++k) fv[k] += __ldcg(p + k);
+                fm = fmax(fm, __ldcg(p + NV));
+            }
+            block_reduce<NV>(fv, fm, S.red);
+            if (threadIdx.x == 0) S.fin[0] = fv[0];
+            __syncthreads();
+        } else {  // counter only (no partial exchange): pure barrier cost
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
+                res_wait(bar, (phase + 1) * gridDim.x);
+            }
+            ++phase;
+            __syncthreads();
+        }
+        acc += S.fin[0] * 1e-9;
+    }
+    if (threadIdx.x == 0 && blockIdx.x == 0) out[0] = acc;
+}
+
+template <int NV, int VAR>
+void run(int nsm, const char* name) {
+    double *part, *out;
+    unsigned* bar;
+    cudaMalloc(&part, 2 * nsm * kSlotDoubles * sizeof(double));
+    cudaMalloc(&out, 8);
+    cudaMalloc(&bar, 4);
+    const int n = 2000;
+    void* args[4];
+    int nn = n;
+    args[0] = &nn; args[1] = &part; args[2] = &bar; args[3] = &out;
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0); cudaEventCreate(&e1);
+    for (int rep = 0; rep < 3; ++rep) {
+        cudaMemset(bar, 0, 4);
+        cudaEventRecord(e0);
+        cudaLaunchCooperativeKernel((void*)k_probe<NV, VAR>, nsm, kBlock, args, 0, 0);
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        float ms; cudaEventElapsedTime(&ms, e0, e1);
+        if (rep == 2) printf("%-28s NV=%2d  %.3f us per all-reduce (%s)\n", name, NV, ms * 1e3 / n,
+                             cudaGetErrorString(cudaGetLastError()));
+    }
+}
+
+int main() {
+    int nsm; cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
+    run<12, 1>(nsm, "counter barrier only");
+    run<12, 2>(nsm, "block reduce+write+barrier");
+    run<12, 3>(nsm, "barrier+read+reduce");
+    run<24, 2>(nsm, "block reduce+write+barrier");
+    run<24, 3>(nsm, "barrier+read+reduce");
+    run<6, 0>(nsm, "allreduce");
+    run<12, 0>(nsm, "allreduce");
+    run<24, 0>(nsm, "allreduce");
+    return 0;
+}
