@@ -321,7 +321,8 @@ def main():
                        "parallelism": f"theta-sharded x{world}",
                        "l2": f"inputs larger than L2 (state {bytes_state / 2**20:.0f} MiB per buffer, "
                              f"2 buffers)",
-                       "schedule": "recompute" if a.schedule == 0 else "stash-half2"},
+                       "schedule": "recompute" if a.schedule == 0 else "stash-P",
+                       "launch": LAUNCH_NAMES.get(eng.launch_mode, str(eng.launch_mode))},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": bytes_state / e2e_steps,
                     "d2h_bytes_per_step": bytes_state / e2e_steps,
                     "call": "osc_set_state(host) + osc_run(Ts=K) + osc_get_state(host)",
@@ -336,6 +337,11 @@ def main():
     eng.close()
     if dist is not None:
         dist.destroy_process_group()
+
+
+LAUNCH_NAMES = {0: "stage kernels, PDL, CUDA graphs of 8 steps",
+                1: "persistent streaming kernel",
+                2: "resident kernel (state in shared memory, grid all-reduce per stage)"}
 
 
 def _other_config(name: str, device: int, no_cpu: bool) -> dict:
@@ -365,9 +371,11 @@ def _other_config(name: str, device: int, no_cpu: bool) -> dict:
     e1.synchronize()
     ms = e0.elapsed_time(e1)
     q = eng.query()
+    launch = LAUNCH_NAMES.get(eng.launch_mode, str(eng.launch_mode))
     eng.close()
     out = {"value": env.cells * steps / (ms * 1e-3), "unit": UNIT, "ms_per_step": ms / steps,
-           "cells": env.cells, "flavours": env.nflav, "steps_timed": steps, "status": q["status"]}
+           "cells": env.cells, "flavours": env.nflav, "steps_timed": steps, "status": q["status"],
+           "launch": launch}
     if no_cpu:
         return out
     try:

@@ -25,3 +25,16 @@ tot = sum(c.values())
 print(lines[0])
 print(f"warp instructions {tot:.4g}")
 print(", ".join(f"{k} {v/tot*100:.1f}%" for k, v in c.most_common(25)))
+
+# executed FP64 thread instructions (DFMA/DMUL/DADD/DSETP/DMNMX...) per launch
+pt = ci["Predicated-On Thread Instructions Executed"]
+fp64 = 0.0
+for r in data:
+    t = r[ci["Source"]].split()
+    if not t:
+        continue
+    o = (t[1] if t[0].startswith("@") else t[0]).split(".")[0]
+    if o in ("DFMA", "DMUL", "DADD", "DSETP", "DMNMX", "DMMA"):
+        fp64 += float(r[pt] or 0)
+cells = float(sys.argv[3]) if len(sys.argv) > 3 else 0
+print(f"fp64 thread instructions {fp64:.4g}" + (f" = {fp64 / cells:.1f} per cell" if cells else ""))
