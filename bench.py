@@ -49,6 +49,7 @@ def _args():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-steps", type=int, default=0)
     ap.add_argument("--no-other-configs", action="store_true")
+    ap.add_argument("--nccl-exchange", action="store_true", help="multi-GPU: NCCL instead of peer stores")
     return ap.parse_args()
 
 
@@ -195,6 +196,19 @@ def main():
 
     env = Environment.from_config(cfg)
     eng = Engine(env, rank=rank, nranks=world, device=local, nccl_id=nccl_id)
+    exchange = "single GPU"
+    if world > 1:
+        # device-initiated stage exchange over NVLink (peer stores of flagged
+        # words); NCCL all-gather if the peers cannot be mapped
+        exchange = "NCCL all-gather per stage"
+        if not a.nccl_exchange:
+            tokens = [None] * world
+            dist.all_gather_object(tokens, eng.comm_export())
+            try:
+                eng.comm_connect(tokens)
+                exchange = "device-initiated peer stores over NVLink"
+            except Exception as e:  # noqa: BLE001
+                print(f"rank {rank}: peer exchange unavailable ({e}); using NCCL", file=sys.stderr)
     if a.schedule >= 0:
         eng.set_schedule(a.schedule)
     eng.init_states()
@@ -319,6 +333,7 @@ def main():
                        "angle_bins": env.abins, "energy_bins": env.ebins, "model": "bulb",
                        "steps_from_r_km": ctl.r, "dr_km": ctl.dr,
                        "parallelism": f"theta-sharded x{world}",
+                       "exchange": exchange,
                        "l2": f"inputs larger than L2 (state {bytes_state / 2**20:.0f} MiB per buffer, "
                              f"2 buffers)",
                        "schedule": "recompute" if a.schedule == 0 else "stash-P",

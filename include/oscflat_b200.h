@@ -91,7 +91,12 @@ typedef struct OscDesc {
 typedef struct OscComm {
     int rank, nranks, device;
     const void* nccl_unique_id; /* 128 bytes, ignored when nranks == 1 */
+    int flags;                  /* OSC_COMM_FORCE_COLLECTIVES: run the multi-GPU
+                                   exchange path (NCCL all-gather + control
+                                   kernel) even when nranks == 1 (tests it on
+                                   one GPU) */
 } OscComm;
+#define OSC_COMM_FORCE_COLLECTIVES 1
 
 /* solver::StepControl (solver.hpp:20-34) */
 typedef struct OscStepControl {
@@ -150,6 +155,16 @@ int osc_version(void);
 
 /* NCCL unique id for a multi-GPU context (rank 0 calls, caller broadcasts). */
 int osc_comm_unique_id(void* out128);
+
+/* Device-initiated exchange (multi-rank contexts): replaces the per-stage NCCL
+ * all-gather by peer stores over NVLink.  Every rank exports 128 bytes (the
+ * CUDA IPC handle of its receive buffer), the caller all-gathers them (rank
+ * order) and hands the nranks x 128 bytes to osc_comm_connect.  The last
+ * block of each stage then stores its rank's moment slot into every rank's
+ * buffer as sequence-flagged 64-bit words (no fences); the consumers poll the
+ * words.  Without connect the NCCL path is used. */
+int osc_comm_export(OscCtx* ctx, void* out128);
+int osc_comm_connect(OscCtx* ctx, const void* handles);
 
 /* Engine(env, lanes) — solver.cpp:459-466 (lanes -> GPUs, one per process). */
 int osc_create(const OscDesc* desc, const OscComm* comm, OscCtx** out);

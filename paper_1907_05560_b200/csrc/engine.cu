@@ -164,6 +164,9 @@ using namespace oscb200;
 struct OscCtx {
     OscDesc desc{};
     int rank = 0, nranks = 1, device = 0;
+    bool coll = false;  // multi-rank exchange path (nranks > 1, or forced for testing)
+    DevBuf<unsigned long long> xll;    // device-initiated exchange receive buffer [4][kMaxRanks][kLLWords]
+    std::vector<void*> ipc_opened;     // peer mappings to close
     int t_lo = 0, t_hi = 0;
     int T = 0, P = 0, E = 0;
     int ntraj = 0, ncell = 0, npad = 0;
@@ -215,6 +218,7 @@ struct OscCtx {
             } catch (...) {
             }
         }
+        for (void* p : ipc_opened) cudaIpcCloseMemHandle(p);
         if (h_ctl) cudaFreeHost(h_ctl);
         for (double* p : pinned)
             if (p) cudaFreeHost(p);
@@ -242,7 +246,7 @@ struct OscCtx {
     }
 
     void exchange(int slot) {
-        if (nranks == 1) return;
+        if (!coll || args.p2p) return;
         nccl::check(nccl::api().all_gather(xsend.p + (size_t)slot * kSlotDoubles,
                                            xbuf.p + (size_t)slot * nranks * kSlotDoubles, kSlotDoubles,
                                            nccl::kFloat64, comm, stream),
@@ -258,7 +262,7 @@ struct OscCtx {
         exchange(2);
         launch_stage(4);
         exchange(3);
-        if (nranks > 1) {
+        if (coll && !args.p2p) {  // (device-initiated exchange: fused into S4)
             k_control<<<1, 128, 0, stream>>>(args);
             count();
             CUDA_OK(cudaGetLastError());
@@ -478,6 +482,7 @@ int osc_create(const OscDesc* desc, const OscComm* comm, OscCtx** out) {
         c->desc = *desc;
         c->rank = comm ? comm->rank : 0;
         c->nranks = comm ? comm->nranks : 1;
+        c->coll = c->nranks > 1 || (comm && (comm->flags & OSC_COMM_FORCE_COLLECTIVES));
         c->device = comm ? comm->device : 0;
         if (c->nranks < 1 || c->nranks > kMaxRanks || c->rank < 0 || c->rank >= c->nranks)
             throw Error(OSC_ERR_CONFIG, "osc_create: bad rank / nranks");
@@ -527,7 +532,9 @@ int osc_create(const OscDesc* desc, const OscComm* comm, OscCtx** out) {
         CUDA_OK(cudaMemset(c->psi[1].p, 0, plane * sizeof(double)));
         c->xbuf.alloc((size_t)4 * c->nranks * kSlotDoubles);
         CUDA_OK(cudaMemset(c->xbuf.p, 0, c->xbuf.n * sizeof(double)));
-        if (c->nranks > 1) {
+        c->xll.alloc((size_t)4 * kMaxRanks * kLLWords);
+        CUDA_OK(cudaMemset(c->xll.p, 0, c->xll.n * sizeof(unsigned long long)));
+        if (c->coll) {
             c->xsend.alloc((size_t)4 * kSlotDoubles);
             CUDA_OK(cudaMemset(c->xsend.p, 0, c->xsend.n * sizeof(double)));
         }
@@ -584,7 +591,7 @@ int osc_create(const OscDesc* desc, const OscComm* comm, OscCtx** out) {
         c->partials.alloc((size_t)c->nblocks * kSlotDoubles);
 
         // persistent kernels: single GPU, 2 flavours
-        if (c->nranks == 1 && c->nflav == 2) {
+        if (!c->coll && c->nflav == 2) {
             const PersistFn pf = persist_kernel(desc->model);
             const size_t sm = c->persist_smem();
             CUDA_OK(cudaFuncSetAttribute(pf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
@@ -617,10 +624,14 @@ int osc_create(const OscDesc* desc, const OscComm* comm, OscCtx** out) {
             }
         }
 
-        if (c->nranks > 1) {
-            if (!comm->nccl_unique_id) throw Error(OSC_ERR_PARALLEL, "osc_create: missing NCCL unique id");
+        if (c->coll) {
             nccl::UniqueId id;
-            std::memcpy(&id, comm->nccl_unique_id, sizeof id);
+            if (comm->nccl_unique_id) {
+                std::memcpy(&id, comm->nccl_unique_id, sizeof id);
+            } else {
+                if (c->nranks > 1) throw Error(OSC_ERR_PARALLEL, "osc_create: missing NCCL unique id");
+                nccl::check(nccl::api().get_unique_id(&id), "ncclGetUniqueId");
+            }
             nccl::check(nccl::api().comm_init_rank(&c->comm, c->nranks, id, c->rank), "ncclCommInitRank");
         }
 
@@ -637,7 +648,7 @@ int osc_create(const OscDesc* desc, const OscComm* comm, OscCtx** out) {
         a.chunk = c->chunk;
         a.ntr_max = c->ntr_max;
         a.nranks = c->nranks;
-        a.fuse_ctl = c->nranks == 1;
+        a.fuse_ctl = !c->coll;
         a.e_magic = c->e_magic;
         a.e_shift = c->e_shift;
         a.schedule = c->schedule;
@@ -670,7 +681,10 @@ int osc_create(const OscDesc* desc, const OscComm* comm, OscCtx** out) {
         a.psi0_buf[1] = c->psi[1].p;
         a.stash = c->stash.p;
         a.xbuf = c->xbuf.p;
-        a.xsend = c->nranks > 1 ? c->xsend.p : c->xbuf.p;
+        a.xsend = c->coll ? c->xsend.p : c->xbuf.p;
+        a.p2p = 0;
+        a.rank = c->rank;
+        a.xll = c->xll.p;
         a.partials = c->partials.p;
         a.ctl = c->ctl.p;
         CUDA_OK(cudaDeviceSynchronize());
@@ -804,7 +818,7 @@ int osc_synchronize(OscCtx* c) {
 
 void* osc_stream(OscCtx* c) { return c ? (void*)c->stream : nullptr; }
 
-int osc_launches_per_step(const OscCtx* c) { return c ? (c->nranks > 1 ? 4 : 3) : 0; }
+int osc_launches_per_step(const OscCtx* c) { return c ? (c->coll && !c->args.p2p ? 4 : 3) : 0; }
 
 int osc_debug_sums(OscCtx* c, double* out) {
     return guarded([&] {
@@ -860,6 +874,45 @@ int osc_set_launch_mode(OscCtx* c, int mode) {
 int osc_get_launch_mode(OscCtx* c) { return c ? c->launch_mode : 0; }
 
 unsigned long long osc_launch_count(const OscCtx* c) { return c ? c->nlaunch : 0; }
+
+int osc_comm_export(OscCtx* c, void* out128) {
+    return guarded([&] {
+        if (!out128) throw Error(OSC_ERR_CONFIG, "osc_comm_export: null out");
+        CUDA_OK(cudaSetDevice(c->device));
+        cudaIpcMemHandle_t h[2];
+        std::memset(h, 0, sizeof h);
+        CUDA_OK(cudaIpcGetMemHandle(&h[0], c->xll.p));  // (second handle reserved)
+        static_assert(sizeof h == 128, "IPC handle size");
+        std::memcpy(out128, h, sizeof h);
+    });
+}
+
+int osc_comm_connect(OscCtx* c, const void* handles) {
+    return guarded([&] {
+        if (!c->coll) throw Error(OSC_ERR_CONFIG, "osc_comm_connect: not a multi-rank context");
+        if (!handles) throw Error(OSC_ERR_CONFIG, "osc_comm_connect: null handles");
+        CUDA_OK(cudaSetDevice(c->device));
+        CUDA_OK(cudaStreamSynchronize(c->stream));
+        StepArgs& a = c->args;
+        for (int q = 0; q < c->nranks; ++q) {
+            if (q == c->rank) {
+                a.peer_xll[q] = c->xll.p;
+                continue;
+            }
+            cudaIpcMemHandle_t h[2];
+            std::memcpy(h, static_cast<const char*>(handles) + (size_t)q * sizeof h, sizeof h);
+            void* pb = nullptr;
+            CUDA_OK(cudaIpcOpenMemHandle(&pb, h[0], cudaIpcMemLazyEnablePeerAccess));
+            c->ipc_opened.push_back(pb);
+            a.peer_xll[q] = static_cast<unsigned long long*>(pb);
+        }
+        a.p2p = 1;
+        if (c->graph) {  // kernel arguments changed
+            cudaGraphExecDestroy(c->graph);
+            c->graph = nullptr;
+        }
+    });
+}
 
 int osc_fp64_peak(int device, double* dfma_per_s, double* ms_out) {
     return guarded([&] {

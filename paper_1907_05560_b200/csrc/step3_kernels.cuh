@@ -119,8 +119,10 @@ __global__ void __launch_bounds__(kBlock, OSC3_MIN_BLOCKS) k_stage3(StepArgs a) 
         if (Tr::hmask & (1 << h)) {
             const int slot = h == 0 ? 0 : (h == 3 ? 2 : 1);
             const int off = h == 2 ? 36 : 0;
+
             // slot layout per set: 9 x geometric moment (a at 0..8, b at 9..17)
             tot[h][k] = slot_total(a, slot, off + k);
+            if (a.p2p && !isfinite(tot[h][k])) atomicOr(&a.ctl->bad_sums, 1);
         }
     }
     if (STAGE == 0 && blockIdx.x == 0 && tid == 0) {
@@ -306,6 +308,7 @@ __global__ void __launch_bounds__(kBlock, OSC3_MIN_BLOCKS) k_stage3(StepArgs a) 
     __syncthreads();
     block_reduce<NV>(fv, fm, red);
     __shared__ double fin[2 * kNM3Max + 1];
+    __shared__ double pub[kSlotDoubles];
     if (tid == 0) {
 #pragma unroll
         for (int k = 0; k < NV; ++k) fin[k] = fv[k];
@@ -327,11 +330,16 @@ __global__ void __launch_bounds__(kBlock, OSC3_MIN_BLOCKS) k_stage3(StepArgs a) 
         } else if (k == 36) {
             v = fin[NV];
         }
-        a.xsend[(size_t)Tr::slot * kSlotDoubles + k] = v;
-        if (STAGE != 4 && !isfinite(v)) atomicOr(&a.ctl->bad_sums, 1);
+        if (!a.p2p) a.xsend[(size_t)Tr::slot * kSlotDoubles + k] = v;
+        if (!a.p2p && STAGE != 4 && !isfinite(v)) atomicOr(&a.ctl->bad_sums, 1);
+        pub[k] = v;
+    }
+    if (a.p2p) {
+        __syncthreads();
+        p2p_publish(a, Tr::slot, tid < kSlotDoubles ? pub[tid] : 0.0);
     }
     if (tid == 0) a.ctl->counter[Tr::slot] = 0;
-    if (STAGE == 4 && a.fuse_ctl) {
+    if (STAGE == 4 && (a.fuse_ctl || a.p2p)) {
         __threadfence();
         __syncthreads();
         control_update(a, true);

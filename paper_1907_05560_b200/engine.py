@@ -184,11 +184,12 @@ class Engine:
     (make_partitions); ``nccl_id`` is the 128-byte id shared by all ranks."""
 
     def __init__(self, env: Environment, rank: int = 0, nranks: int = 1, device: int = 0,
-                 nccl_id: bytes | None = None):
+                 nccl_id: bytes | None = None, force_collectives: bool = False):
         self.env = env  # borrowed, kept alive (solver.hpp:152)
         self._idbuf = C.create_string_buffer(nccl_id, 128) if nccl_id else None
         comm = OscComm(rank=rank, nranks=nranks, device=device,
-                       nccl_unique_id=C.cast(self._idbuf, C.c_void_p) if self._idbuf else None)
+                       nccl_unique_id=C.cast(self._idbuf, C.c_void_p) if self._idbuf else None,
+                       flags=native.COMM_FORCE_COLLECTIVES if force_collectives else 0)
         self._ctx = C.c_void_p()
         check(lib().osc_create(C.byref(env.desc), C.byref(comm), C.byref(self._ctx)))
         lo, hi, n = C.c_int(), C.c_int(), C.c_size_t()
@@ -327,6 +328,18 @@ class Engine:
 
     def set_schedule(self, schedule: int) -> None:
         check(lib().osc_set_schedule(self._ctx, schedule))
+
+    def comm_export(self) -> bytes:
+        """128-byte token (CUDA IPC handles of this rank's exchange slots)."""
+        buf = C.create_string_buffer(128)
+        check(lib().osc_comm_export(self._ctx, buf))
+        return buf.raw
+
+    def comm_connect(self, tokens) -> None:
+        """Switch the stage exchange from NCCL to device-initiated peer stores;
+        tokens = every rank's comm_export() in rank order."""
+        blob = b"".join(tokens)
+        check(lib().osc_comm_connect(self._ctx, C.create_string_buffer(blob, len(blob))))
 
     LAUNCH_STAGES, LAUNCH_PERSISTENT, LAUNCH_RESIDENT = 0, 1, 2
 

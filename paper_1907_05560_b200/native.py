@@ -27,7 +27,10 @@ class OscDesc(C.Structure):
 
 class OscComm(C.Structure):
     _fields_ = [("rank", C.c_int), ("nranks", C.c_int), ("device", C.c_int),
-                ("nccl_unique_id", C.c_void_p)]
+                ("nccl_unique_id", C.c_void_p), ("flags", C.c_int)]
+
+
+COMM_FORCE_COLLECTIVES = 1
 
 
 class OscStepControl(C.Structure):
@@ -83,7 +86,7 @@ SYMBOLS = [
     "osc_local_range", "osc_init_states", "osc_set_state", "osc_get_state",
     "osc_set_state_device", "osc_get_state_device", "osc_trial_step_error", "osc_run", "osc_run_dumps", "osc_extract_mode2",
     "osc_max_norm_dev", "osc_begin", "osc_enqueue_steps", "osc_query", "osc_synchronize",
-    "osc_stream", "osc_launches_per_step", "osc_debug_sums", "osc_set_schedule", "osc_set_launch_mode", "osc_get_launch_mode", "osc_launch_count",
+    "osc_stream", "osc_launches_per_step", "osc_debug_sums", "osc_set_schedule", "osc_set_launch_mode", "osc_get_launch_mode", "osc_comm_export", "osc_comm_connect", "osc_launch_count",
     "osc_fp64_peak", "osc_profile_stages", "osc_env_build", "osc_env_desc", "osc_env_destroy", "osc_fermi_integral",
 ]
 
@@ -126,6 +129,8 @@ def lib() -> C.CDLL:
     L.osc_debug_sums.argtypes = [vp, _dp]
     L.osc_set_schedule.argtypes = [vp, C.c_int]
     L.osc_set_launch_mode.argtypes = [vp, C.c_int]
+    L.osc_comm_export.argtypes = [vp, vp]
+    L.osc_comm_connect.argtypes = [vp, vp]
     L.osc_get_launch_mode.argtypes = [vp]
     L.osc_launch_count.argtypes = [vp]
     L.osc_launch_count.restype = C.c_ulonglong

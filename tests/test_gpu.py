@@ -514,3 +514,34 @@ def test_mode2_three_flavour_is_electron_probability_average():
     got = eng.mode2().reshape(-1, 6)
     want = np.einsum("tse,se->ts", x[:, :, 0] ** 2 + x[:, :, 1] ** 2, fw)
     assert np.max(np.abs(got - want)) <= 1e-13 * np.max(np.abs(want))
+
+
+@pytest.mark.parametrize("model,p2p", [("bulb", False), ("ebulb", False), ("bulb", True),
+                                       ("ebulb", True), ("flavour3", True)])
+def test_collective_path_on_one_gpu_matches_fused_path(model, p2p):
+    """The multi-GPU exchange path (NCCL all-gather of the stage partials into
+    the rank slots, the one-block control kernel, unfused sums check) run with
+    a one-rank communicator must reproduce the single-GPU path bit for bit —
+    the NCCL plumbing and k_control exercised on hardware."""
+    if model == "flavour3":
+        cfg = baseline_config("configs1", Abins=16, Ebins=8, R0=50, Rn=60, Ts=12, dr=1e-4, max_dr=1e-4)
+    else:
+        cfg = baseline_config("configs0", Abins=24, Ebins=20, Ts=30, dr=0.5, max_dr=0.5, eps0=1e-9)
+    if model == "ebulb":
+        cfg.override("model=ebulb").override("Pbins=8").override("perturb=1e-6")
+    out = []
+    for coll in (False, True):
+        env = Environment.from_config(cfg)
+        eng = Engine(env, force_collectives=coll)
+        eng.init_states()
+        if coll and p2p:  # device-initiated exchange, this rank as its own peer
+            eng.comm_connect([eng.comm_export()])
+        if not coll and env.nflav == 2:
+            eng.set_launch_mode(Engine.LAUNCH_STAGES)
+        assert eng.launches_per_step() == (4 if coll and not p2p else 3)
+        s = eng.run(StepControl.from_config(cfg))
+        out.append((s.iterations, s.accepted, s.rejected, s.final_r, eng.state()))
+    (ia, aa, ra, fa, sa), (ib, ab, rb, fb, sb) = out
+    assert (ia, aa, ra, fa) == (ib, ab, rb, fb) and ia > 0
+    assert ra > 0 or model == "flavour3"
+    assert np.array_equal(sa, sb)
