@@ -211,14 +211,11 @@ __global__ void __launch_bounds__(kBlock, 1)
                 Prop um[2], uf[2];
                 const PropReq rq[2] = {{R->hb[0], R->dl[0], false, um}, {R->hb[0], R->dl[2], false, uf}};
                 make_props_n(K, rq);
-                double y[4][4], Rr[3];
-#pragma unroll
-                for (int s = 0; s < 4; ++s) apply(um[s & 1], x[s], y[s]);
-                weighted_rho(y, K, Rr);
+                double B[2][3], Rr[3];
+                class_bloch(x, K, B);
+                bloch_rho(um, B, Rr);
                 fold_acc<NM>(acc + NM, Rr, R->fold[1]);
-#pragma unroll
-                for (int s = 0; s < 4; ++s) apply(uf[s & 1], x[s], y[s]);
-                weighted_rho(y, K, Rr);
+                bloch_rho(uf, B, Rr);
                 fold_acc<NM>(acc, Rr, R->fold[0]);
             }
             if (!res_allreduce<2 * NM>(acc, 0.0, part, bar, phase, S, S.fin)) break;
