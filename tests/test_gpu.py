@@ -545,3 +545,31 @@ def test_collective_path_on_one_gpu_matches_fused_path(model, p2p):
     assert (ia, aa, ra, fa) == (ib, ab, rb, fb) and ia > 0
     assert ra > 0 or model == "flavour3"
     assert np.array_equal(sa, sb)
+
+
+DROPIN = os.path.join(os.path.dirname(os.path.dirname(__file__)), "integration", "_build", "oscflat_b200_dropin")
+
+
+@pytest.mark.skipif(not os.path.exists(DROPIN), reason="drop-in binary not built (integration/Makefile)")
+@pytest.mark.parametrize("name", ["bulb_resolved", "ebulb_resolved", "bulb_adaptive_matter"])
+def test_reference_host_code_with_engine_replaced(golden, cases, name, tmp_path):
+    """The reference's own run path (config parsing, Environment, StepControl,
+    Engine API, extract_mode1, RunSummary::to_kv — compiled from the reference
+    sources) linked with solver::Engine replaced by the C-ABI shim
+    (integration/solver_b200.cpp): same final state and step counts as the
+    unmodified reference (golden)."""
+    import subprocess
+
+    cfg_path = tmp_path / "run.cfg"
+    cfg_path.write_text(cases[name].render())
+    out_path = tmp_path / "state.bin"
+    r = subprocess.run([DROPIN, str(cfg_path), str(out_path), "4"], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr
+    kv = dict(line.split("= ", 1) for line in r.stdout.splitlines() if "= " in line)
+    summ = golden[f"{name}/summary"]
+    assert int(kv["iterations"]) == int(summ[1]) and int(kv["accepted"]) == int(summ[2])
+    assert float(kv["final_r"]) == pytest.approx(summ[0], rel=1e-14)
+    got = np.fromfile(out_path, dtype=np.float64)
+    want = golden[f"{name}/final_state"]
+    assert got.shape == want.shape
+    assert np.max(np.abs(got - want)) <= 1e-12
