@@ -93,3 +93,16 @@ def test_bad_descriptor_is_config_error():
     ctx = C.c_void_p()
     rc = native.lib().osc_create(C.byref(d2), None, C.byref(ctx))
     assert rc == 1  # OSC_ERR_CONFIG, raised before any device call
+
+
+@pytest.mark.skipif(not os.path.isdir("/root/reference/proj/core/include"), reason="reference headers absent")
+def test_engine_shim_compiles_against_reference_headers():
+    """integration/solver_b200.cpp implements the reference's solver::Engine
+    declaration (solver.hpp:128-153) over include/oscflat_b200.h."""
+    import subprocess
+
+    r = subprocess.run(["g++", "-std=gnu++20", "-fsyntax-only", "-include", "cstdint",
+                        "-I", "/root/reference/proj/core/include", "-I", os.path.join(ROOT, "include"),
+                        os.path.join(ROOT, "integration", "solver_b200.cpp")],
+                       capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
