@@ -50,23 +50,29 @@ __device__ __forceinline__ bool res_wait(const unsigned* bar, unsigned target) {
     return false;
 }
 
-// Grid all-reduce of NV sums + 1 max.  Block partial (fixed tree) ->
-// part[phase & 1][block] -> release arrival -> acquire wait -> every block
-// sums all partials in the same fixed order.  out[0..NV] = totals, max.
+// Grid all-reduce of NV sums + 1 max, in two halves so independent work can
+// run while the other blocks arrive.  res_arrive: block partial (fixed tree)
+// -> part[phase & 1][value][block] -> release arrival.  res_finish: acquire
+// wait -> every block sums all partials in the same fixed order ->
+// out[0..NV] = totals, max.
 template <int NV>
-__device__ __forceinline__ bool res_allreduce(double (&v)[NV], double mx, double* part, unsigned* bar,
-                                              unsigned& phase, ResShared& S, double* out) {
-    const int tid = threadIdx.x;
+__device__ __forceinline__ void res_arrive(double (&v)[NV], double mx, double* part, unsigned* bar,
+                                           unsigned phase, ResShared& S) {
     block_reduce<NV>(v, mx, S.red);
-    double* slot = part + (size_t)(phase & 1) * gridDim.x * kSlotDoubles;
-    if (tid == 0) {  // [value][block] layout: the reads below coalesce
-        double* p = slot + blockIdx.x;
+    if (threadIdx.x == 0) {  // [value][block] layout: the reads coalesce
+        double* p = part + (size_t)(phase & 1) * gridDim.x * kSlotDoubles + blockIdx.x;
 #pragma unroll
         for (int k = 0; k < NV; ++k) p[(size_t)k * gridDim.x] = v[k];
         p[(size_t)NV * gridDim.x] = mx;
         asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
-        S.stop = res_wait(bar, (phase + 1) * gridDim.x) ? 0 : 1;
     }
+}
+template <int NV>
+__device__ __forceinline__ bool res_finish(double* part, unsigned* bar, unsigned& phase, ResShared& S,
+                                           double* out) {
+    const int tid = threadIdx.x;
+    if (tid == 0) S.stop = res_wait(bar, (phase + 1) * gridDim.x) ? 0 : 1;
+    const double* slot = part + (size_t)(phase & 1) * gridDim.x * kSlotDoubles;
     ++phase;
     __syncthreads();
     if (S.stop) return false;
@@ -90,10 +96,20 @@ __device__ __forceinline__ bool res_allreduce(double (&v)[NV], double mx, double
     __syncthreads();
     return true;
 }
+template <int NV>
+__device__ __forceinline__ bool res_allreduce(double (&v)[NV], double mx, double* part, unsigned* bar,
+                                              unsigned& phase, ResShared& S, double* out) {
+    res_arrive<NV>(v, mx, part, bar, phase, S);
+    return res_finish<NV>(part, bar, phase, S, out);
+}
+
+// Per-cell propagators carried between the stages of a step ([24][ch]):
+// Um (S2 -> S3), Uf then Q = (Uf + U2)/2 (S2 -> S4), P (S3 -> S4).
+constexpr int kResProps = 24;
 
 // Shared-memory bytes of the resident kernel for a chunk of `ch` cells.
 inline size_t resident_smem_bytes(int ch, int ntr_max, int E) {
-    return (size_t)(2 * kPlanes + kStashPlanes) * ch * sizeof(double) + (size_t)ntr_max * sizeof(TrajRec) +
+    return (size_t)(2 * kPlanes + kResProps) * ch * sizeof(double) + (size_t)ntr_max * sizeof(TrajRec) +
            (size_t)6 * E * sizeof(double);
 }
 
@@ -113,7 +129,23 @@ __global__ void __launch_bounds__(kBlock, 1)
     const size_t np = a.npad;
     double* buf[2] = {reinterpret_cast<double*>(dsm), reinterpret_cast<double*>(dsm) + (size_t)kPlanes * ch};
     double* pst = buf[1] + (size_t)kPlanes * ch;
-    TrajRec* rec = reinterpret_cast<TrajRec*>(pst + (size_t)kStashPlanes * ch);
+    TrajRec* rec = reinterpret_cast<TrajRec*>(pst + (size_t)kResProps * ch);
+    // pst rows: 0-7 Um, 8-15 Uf -> Q, 16-23 P (class c at 4 c + {c, a, b, d})
+    auto put = [&](int row, int k, const Prop (&u)[2]) {
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+            pst[(size_t)(row + 4 * c + 0) * ch + k] = u[c].c;
+            pst[(size_t)(row + 4 * c + 1) * ch + k] = u[c].a;
+            pst[(size_t)(row + 4 * c + 2) * ch + k] = u[c].b;
+            pst[(size_t)(row + 4 * c + 3) * ch + k] = u[c].d;
+        }
+    };
+    auto get = [&](int row, int k, Prop (&u)[2]) {
+#pragma unroll
+        for (int c = 0; c < 2; ++c)
+            u[c] = Prop{pst[(size_t)(row + 4 * c + 0) * ch + k], pst[(size_t)(row + 4 * c + 1) * ch + k],
+                        pst[(size_t)(row + 4 * c + 2) * ch + k], pst[(size_t)(row + 4 * c + 3) * ch + k]};
+    };
     double* ktab = reinterpret_cast<double*>(rec + ntr_cap);
 
     grid_dependency_wait();
@@ -217,6 +249,8 @@ __global__ void __launch_bounds__(kBlock, 1)
                 fold_acc<NM>(acc + NM, Rr, R->fold[1]);
                 bloch_rho(uf, B, Rr);
                 fold_acc<NM>(acc, Rr, R->fold[0]);
+                put(0, k, um);
+                put(8, k, uf);
             }
             if (!res_allreduce<2 * NM>(acc, 0.0, part, bar, phase, S, S.fin)) break;
             if (tid < 2 * NM) S.tot1[tid] = S.fin[tid];
@@ -233,7 +267,8 @@ __global__ void __launch_bounds__(kBlock, 1)
         }
         __syncthreads();
 
-        // ---- S3: half2 = P psi0 with P = Uh(H2) Um(H0); sums3 at r+dr
+        // ---- S3: half2 = P psi0 with P = Uh(H2) Um(H0); sums3 at r+dr.  While
+        // the other blocks arrive: U2(H1) and Q = (Uf + U2)/2 for S4.
         {
             double acc[NM];
 #pragma unroll
@@ -243,22 +278,40 @@ __global__ void __launch_bounds__(kBlock, 1)
                 double x[4][4];
                 const TrajRec* R;
                 load_cell(k, K, x, R);
-                Prop P[2];
-                make_half2_prop(K, *R, P);
+                Prop uh[2], um[2], P[2];
+                {
+                    const PropReq rq[1] = {{R->hb[2], R->dl[1], false, uh}};
+                    make_props_n(K, rq);
+                }
+                get(0, k, um);
+                P[0] = prop_mul(uh[0], um[0]);
+                P[1] = prop_mul(uh[1], um[1]);
                 double hh[4][4], Rr[3];
 #pragma unroll
                 for (int s = 0; s < 4; ++s) apply(P[s & 1], x[s], hh[s]);
                 weighted_rho(hh, K, Rr);
                 fold_acc<NM>(acc, Rr, R->fold[0]);
-#pragma unroll
-                for (int c = 0; c < 2; ++c) {
-                    pst[(size_t)(c * 4 + 0) * ch + k] = P[c].c;
-                    pst[(size_t)(c * 4 + 1) * ch + k] = P[c].a;
-                    pst[(size_t)(c * 4 + 2) * ch + k] = P[c].b;
-                    pst[(size_t)(c * 4 + 3) * ch + k] = P[c].d;
-                }
+                put(16, k, P);
             }
-            if (!res_allreduce<NM>(acc, 0.0, part, bar, phase, S, S.fin)) break;
+            res_arrive<NM>(acc, 0.0, part, bar, phase, S);
+            for (int k = tid; k < n; k += kBlock) {
+                CellK K;
+                double x[4][4];
+                const TrajRec* R;
+                load_cell(k, K, x, R);
+                Prop u2[2], uf[2], Q[2];
+                {
+                    const PropReq rq[1] = {{R->hb[1], R->dl[2], true, u2}};
+                    make_props_n(K, rq);
+                }
+                get(8, k, uf);
+#pragma unroll
+                for (int c = 0; c < 2; ++c)
+                    Q[c] = Prop{fma(uf[c].c, 0.5, u2[c].c), fma(uf[c].a, 0.5, u2[c].a), fma(uf[c].b, 0.5, u2[c].b),
+                                fma(uf[c].d, 0.5, u2[c].d)};
+                put(8, k, Q);
+            }
+            if (!res_finish<NM>(part, bar, phase, S, S.fin)) break;
             if (tid < NM) S.tot3[tid] = S.fin[tid];
         }
         // H3 (sums3, r+dr)
@@ -283,23 +336,19 @@ __global__ void __launch_bounds__(kBlock, 1)
                 double x[4][4];
                 const TrajRec* R;
                 load_cell(k, K, x, R);
-                Prop u3[2], u1[2], u2[2];
+                Prop u3[2], P[2], Q[2];
                 {
-                    const PropReq rq[2] = {{R->hb[0], R->dl[2], false, u1}, {R->hb[1], R->dl[2], true, u2}};
-                    make_props_n(K, rq);
                     const PropReq rq3[1] = {{R->hb[3], R->dl[2], true, u3}};
                     make_props_n(K, rq3);
                 }
+                get(16, k, P);
+                get(8, k, Q);
                 Prop Rm[2], Dm[2];
 #pragma unroll
                 for (int c = 0; c < 2; ++c) {
-                    const Prop P{pst[(size_t)(c * 4 + 0) * ch + k], pst[(size_t)(c * 4 + 1) * ch + k],
-                                 pst[(size_t)(c * 4 + 2) * ch + k], pst[(size_t)(c * 4 + 3) * ch + k]};
-                    const Prop Q{fma(u1[c].c, 0.5, u2[c].c), fma(u1[c].a, 0.5, u2[c].a), fma(u1[c].b, 0.5, u2[c].b),
-                                 fma(u1[c].d, 0.5, u2[c].d)};
-                    Rm[c] = Prop{fma(P.c, 0.5, u3[c].c), fma(P.a, 0.5, u3[c].a), fma(P.b, 0.5, u3[c].b),
-                                 fma(P.d, 0.5, u3[c].d)};
-                    Dm[c] = Prop{Q.c - Rm[c].c, Q.a - Rm[c].a, Q.b - Rm[c].b, Q.d - Rm[c].d};
+                    Rm[c] = Prop{fma(P[c].c, 0.5, u3[c].c), fma(P[c].a, 0.5, u3[c].a), fma(P[c].b, 0.5, u3[c].b),
+                                 fma(P[c].d, 0.5, u3[c].d)};
+                    Dm[c] = Prop{Q[c].c - Rm[c].c, Q[c].a - Rm[c].a, Q[c].b - Rm[c].b, Q[c].d - Rm[c].d};
                 }
                 double Rr[3] = {0.0, 0.0, 0.0};
 #pragma unroll
