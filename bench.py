@@ -302,6 +302,12 @@ def main():
                 "W_per_cell": w_k, "W_source": W["source"],
                 "peak_source": "measured live: DFMA-chain microkernel (osc_fp64_peak)",
                 "stage_ms": dict(zip(names, stage_ms)),
+                "hbm_view": ({"bytes_per_launch": W["traffic"][names[k]],
+                              "achieved_gbs": W["traffic"][names[k]] / (stage_ms[k] * 1e-3) / 1e9,
+                              "frac": W["traffic"][names[k]] / (stage_ms[k] * 1e-3) / 1e9 / hbm_peak[0],
+                              "note": "the same kernel against the HBM roof: ncu-measured DRAM bytes "
+                                      "per launch over its live duration"}
+                             if W.get("traffic", {}).get(names[k]) else None),
                 "step": {"W_per_cell": w_step, "achieved": step_achieved,
                          "frac_fp64": step_achieved / peak,
                          "hbm_compulsory_gbs": 256 * cells_total / (ms / a.steps * 1e-3) / 1e9,
