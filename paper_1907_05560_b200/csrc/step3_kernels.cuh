@@ -201,7 +201,9 @@ __global__ void __launch_bounds__(kBlock, OSC3_MIN_BLOCKS) k_stage3(StepArgs a) 
 #pragma unroll
                 for (int k = 0; k < 9; ++k) acc[9 * j + k] += R.fold[0][j] * Rr[k];
         } else if (STAGE == 2) {
-            const Mat3 um = prop(0, 0), uf = prop(0, 2);
+            // mid and full1 share H0: one eigendecomposition, two exponentials
+            const Eig3 e0 = eig_herm3(herm_of(v, R.hb[0], pc));
+            const Mat3 um = exp_from_eig(e0, R.dl[0]), uf = exp_from_eig(e0, R.dl[2]);
             double y[3][6];
 #pragma unroll
             for (int f = 0; f < 3; ++f) apply3(um, x[f], y[f]);
