@@ -286,10 +286,9 @@ __global__ void __launch_bounds__(kBlock, 1)
                 get(0, k, um);
                 P[0] = prop_mul(uh[0], um[0]);
                 P[1] = prop_mul(uh[1], um[1]);
-                double hh[4][4], Rr[3];
-#pragma unroll
-                for (int s = 0; s < 4; ++s) apply(P[s & 1], x[s], hh[s]);
-                weighted_rho(hh, K, Rr);
+                double B[2][3], Rr[3];
+                class_bloch(x, K, B);
+                bloch_rho(P, B, Rr);
                 fold_acc<NM>(acc, Rr, R->fold[0]);
                 put(16, k, P);
             }
