@@ -34,6 +34,29 @@ def to_num(s):
         return s
 
 
+def fp64_from_source(rep: str, idx: int):
+    """Predicated-on thread instructions of FP64-pipe opcodes of launch idx."""
+    out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass",
+                          "--launch-skip", str(idx), "--launch-count", "1"], capture_output=True,
+                         text=True).stdout.splitlines()
+    try:
+        h0 = next(i for i, ln in enumerate(out) if ln.startswith('"Address"'))
+    except StopIteration:
+        return None
+    rows = list(csv.reader(io.StringIO("\n".join(out[h0:]))))
+    ci = {h: i for i, h in enumerate(rows[0])}
+    data = [r for r in rows[1:] if r and r[0].startswith("0x")]
+    if len(data) % 2 == 0 and data[:len(data) // 2] == data[len(data) // 2:]:
+        data = data[:len(data) // 2]
+    tot = 0.0
+    for r in data:
+        t = r[ci["Source"]].split()
+        if t and (t[1] if t[0].startswith("@") else t[0]).split(".")[0] in ("DFMA", "DMUL", "DADD", "DSETP",
+                                                                          "DMNMX"):
+            tot += float(r[ci["Predicated-On Thread Instructions Executed"]] or 0)
+    return tot
+
+
 def main():
     rep, out = sys.argv[1], sys.argv[2]
     cells = float(sys.argv[3]) if len(sys.argv) > 3 else 1048576.0
@@ -55,6 +78,8 @@ def main():
                 if k.startswith("dram_") and k != "dram_pct":
                     v = v * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(u, 1)
                 d[k] = v
+        if not isinstance(d.get("fp64_all"), float):  # not in --set full: count from the SASS page
+            d["fp64_all"] = fp64_from_source(rep, len(res))
         if isinstance(d.get("fp64_all"), float):
             d["fp64_per_cell"] = d["fp64_all"] / cells
         if isinstance(d.get("dram_read"), float):
