@@ -194,7 +194,7 @@ struct OscCtx {
     cudaStream_t stream = nullptr;
     nccl::Comm comm = nullptr;
 
-    DevBuf<double> cos2, sin0, cphi, sphi, vac11, vac12, g;
+    DevBuf<double> cos2, sin0, cphi, sphi, vac11, vac12, g, ktab_g;
     DevBuf<double> psi[2], stash, xbuf, xsend, partials, staging;
     // snapshot I/O: spectrum weights [nsp][E] (mode 2), mode-2 output, the
     // second packing buffer and pinned host buffers of the async dumps
@@ -523,6 +523,13 @@ int osc_create(const OscDesc* desc, const OscComm* comm, OscCtx** out) {
             for (int e = 0; e < c->E; ++e)
                 g[(size_t)s * c->E + e] = ((s & 1) ? -1.0 : 1.0) * cpl[s] * fw[(size_t)s * c->E + e];
         upload(c->g, g.data(), g.size());
+        if (c->nflav == 2) {  // contiguous per-energy table for the stage kernels' bulk copy
+            std::vector<double> kt((size_t)((6 * c->E + 1) & ~1), 0.0);
+            std::copy(desc->vac_h11, desc->vac_h11 + c->E, kt.begin());
+            std::copy(desc->vac_h12, desc->vac_h12 + c->E, kt.begin() + c->E);
+            std::copy(g.begin(), g.end(), kt.begin() + 2 * (size_t)c->E);
+            upload(c->ktab_g, kt.data(), kt.size());
+        }
         upload(c->fw, fw, (size_t)nsp * c->E);
         if (c->nflav == 3) upload(c->vac3, desc->vac3, 9 * (size_t)c->E);
         const size_t plane = (size_t)c->npad * c->nplanes;
@@ -667,6 +674,7 @@ int osc_create(const OscDesc* desc, const OscComm* comm, OscCtx** out) {
         a.vac11 = c->vac11.p;
         a.vac12 = c->vac12.p;
         a.g = c->g.p;
+        a.ktab = c->ktab_g.p;
         a.vac3 = c->vac3.p;
         a.nmom = c->nflav == 3 ? 36 : 12;
         a.nplanes = c->nplanes;
