@@ -361,7 +361,6 @@ def main():
 
 
 LAUNCH_NAMES = {0: "stage kernels, PDL, CUDA graphs of 8 steps",
-                1: "persistent streaming kernel",
                 2: "resident kernel (state in shared memory, grid all-reduce per stage)"}
 
 

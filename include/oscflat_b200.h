@@ -232,11 +232,11 @@ int osc_set_schedule(OscCtx* ctx, int schedule);
 /* How step batches launch (single-GPU 2-flavour contexts; multi-GPU and
  * 3-flavour contexts always use 0):
  *   0  stage kernels with programmatic dependent launch, CUDA graphs of 8 steps;
- *   1  one persistent cooperative kernel streaming the state from HBM, grid
- *      barriers between stages (opt-in; measured slower than 0);
  *   2  one persistent cooperative kernel with the whole local state resident
  *      in shared memory (default when it fits: small problems, configs[0]).
- * Env OSC_LAUNCH=0/1/2 overrides the default.  OSC_ERR_CONFIG when the mode is
+ * (1, a persistent kernel streaming the state from HBM with grid barriers
+ * between stages, measured slower than 0 on every config and was removed.)
+ * Env OSC_LAUNCH=0/2 overrides the default.  OSC_ERR_CONFIG when the mode is
  * unavailable for this context. */
 int osc_set_launch_mode(OscCtx* ctx, int mode);
 int osc_get_launch_mode(OscCtx* ctx);

@@ -107,17 +107,6 @@ StageFn stage3_fn(int stage) {
         default: return k_stage3<MODEL, 4>;
     }
 }
-using PersistFn = void (*)(StepArgs, int);
-PersistFn persist_kernel(int model) {
-    switch (model) {
-        case 0: return k_persist<0>;
-        case 1: return k_persist<1>;
-        case 2: return k_persist<2>;
-        case 3: return k_persist<3>;
-        default: return k_persist<4>;
-    }
-}
-
 using ResidentFn = void (*)(StepArgs, int, int, int, double*, unsigned*);
 ResidentFn resident_kernel(int model) {
     switch (model) {
@@ -177,9 +166,8 @@ struct OscCtx {
     int nplanes = 16;  // state planes per buffer
     DevBuf<double> vac3;
     int use_pdl = 1;
-    int persist_ok = 0;   // the persistent streaming kernel fits one resident wave
     int resident_ok = 0;  // the whole state fits in shared memory (k_resident)
-    int launch_mode = 0;  // 0 stage kernels + graphs, 1 persistent streaming, 2 resident
+    int launch_mode = 0;  // 0 stage kernels + graphs, 2 resident
     int rch = 0, rntr = 0;
     size_t rsmem = 0;
     DevBuf<double> rpart;
@@ -291,29 +279,6 @@ struct OscCtx {
         graph_steps = steps;
     }
 
-    size_t persist_smem() const {
-        size_t m = 0;
-        for (int st : {2, 3, 4}) m = std::max(m, stage_smem_bytes(st, schedule, ntr_max, E));
-        return m;
-    }
-
-    // n steps in ONE cooperative launch: grid barriers replace the kernel
-    // boundaries (single GPU; every block resident by construction).
-    void launch_persist(int n) {
-        cudaLaunchConfig_t cfg{};
-        cfg.gridDim = dim3(nblocks);
-        cfg.blockDim = dim3(kBlock);
-        cfg.dynamicSmemBytes = persist_smem();
-        cfg.stream = stream;
-        cudaLaunchAttribute attr[1];
-        attr[0].id = cudaLaunchAttributeCooperative;
-        attr[0].val.cooperative = 1;
-        cfg.attrs = attr;
-        cfg.numAttrs = 1;
-        CUDA_OK(cudaLaunchKernelEx(&cfg, persist_kernel(desc.model), args, n));
-        count();
-    }
-
     // n steps in one cooperative launch with the state resident in shared
     // memory (single GPU, small problems).
     void launch_resident(int n) {
@@ -336,10 +301,6 @@ struct OscCtx {
         if (n <= 0) return;
         if (launch_mode == 2) {
             launch_resident(n);
-            return;
-        }
-        if (launch_mode == 1 && n > 1 && schedule == 1) {  // (the persistent kernel reads the stash)
-            launch_persist(n);
             return;
         }
         if (n >= 8) {
@@ -597,14 +558,8 @@ int osc_create(const OscDesc* desc, const OscComm* comm, OscCtx** out) {
         }
         c->partials.alloc((size_t)c->nblocks * kSlotDoubles);
 
-        // persistent kernels: single GPU, 2 flavours
+        // resident kernel: single GPU, 2 flavours
         if (!c->coll && c->nflav == 2) {
-            const PersistFn pf = persist_kernel(desc->model);
-            const size_t sm = c->persist_smem();
-            CUDA_OK(cudaFuncSetAttribute(pf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-            int per_sm = 0;
-            CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pf, kBlock, sm));
-            c->persist_ok = (long)per_sm * c->nsm >= c->nblocks && OSC_DEBUG_MODE == 0;
             // resident: the local state, the result and the stash of a chunk
             // per SM in shared memory
             c->rch = (c->ncell + c->nsm - 1) / c->nsm;
@@ -622,12 +577,11 @@ int osc_create(const OscDesc* desc, const OscComm* comm, OscCtx** out) {
                 }
             }
             // default: resident where the state fits, else the PDL-pipelined
-            // stage kernels (the persistent streaming kernel measured slower);
-            // env OSC_LAUNCH=0/1/2 overrides
+            // stage kernels; env OSC_LAUNCH=0/2 overrides
             c->launch_mode = c->resident_ok ? 2 : 0;
             if (const char* env = std::getenv("OSC_LAUNCH")) {
                 const int m = std::atoi(env);
-                if (m == 0 || (m == 1 && c->persist_ok) || (m == 2 && c->resident_ok)) c->launch_mode = m;
+                if (m == 0 || (m == 2 && c->resident_ok)) c->launch_mode = m;
             }
         }
 
@@ -858,9 +812,6 @@ int osc_set_schedule(OscCtx* c, int schedule) {
         c->schedule = schedule;
         c->args.schedule = schedule;
         c->args.stash = c->stash.p;
-        if (c->persist_ok)
-            CUDA_OK(cudaFuncSetAttribute(persist_kernel(c->desc.model), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)c->persist_smem()));
         if (c->graph) {
             cudaGraphExecDestroy(c->graph);
             c->graph = nullptr;
@@ -870,9 +821,7 @@ int osc_set_schedule(OscCtx* c, int schedule) {
 
 int osc_set_launch_mode(OscCtx* c, int mode) {
     return guarded([&] {
-        if (mode < 0 || mode > 2) throw Error(OSC_ERR_CONFIG, "launch mode must be 0, 1 or 2");
-        if (mode == 1 && !c->persist_ok)
-            throw Error(OSC_ERR_CONFIG, "persistent kernel unavailable (multi-rank, 3 flavours or occupancy)");
+        if (mode != 0 && mode != 2) throw Error(OSC_ERR_CONFIG, "launch mode must be 0 or 2");
         if (mode == 2 && !c->resident_ok)
             throw Error(OSC_ERR_CONFIG, "resident kernel unavailable (multi-rank, 3 flavours or state too large)");
         c->launch_mode = mode;

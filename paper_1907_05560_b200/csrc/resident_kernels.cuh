@@ -399,9 +399,7 @@ __global__ void __launch_bounds__(kBlock, 1)
                 S.c.reason = 4;
                 S.c.terminate = 4;
             }
-            Ctl* gc = a.ctl;
-            S.c.bar_gen = gc->bar_gen;
-            *gc = S.c;
+            *a.ctl = S.c;
         }
     }
 }

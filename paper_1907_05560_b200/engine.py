@@ -341,12 +341,12 @@ class Engine:
         blob = b"".join(tokens)
         check(lib().osc_comm_connect(self._ctx, C.create_string_buffer(blob, len(blob))))
 
-    LAUNCH_STAGES, LAUNCH_PERSISTENT, LAUNCH_RESIDENT = 0, 1, 2
+    LAUNCH_STAGES, LAUNCH_RESIDENT = 0, 2
 
     def set_launch_mode(self, mode: int) -> None:
-        """0: stage kernels (PDL, CUDA graphs); 1: persistent streaming kernel;
-        2: persistent kernel with the state resident in shared memory (the
-        default where it fits).  Raises ConfigError if unavailable."""
+        """0: stage kernels (PDL, CUDA graphs); 2: persistent kernel with the
+        state resident in shared memory (the default where it fits).  Raises
+        ConfigError if unavailable."""
         check(lib().osc_set_launch_mode(self._ctx, int(mode)))
 
     @property

@@ -412,10 +412,11 @@ def test_three_flavour_decoupled_tau_equals_two_flavour_gpu():
 
 
 @pytest.mark.parametrize("model", ["sa", "bulb", "ebulb", "plane", "cylinder"])
-def test_persistent_kernel_bit_identical_to_stage_kernels(model):
-    """The persistent cooperative kernel (grid barriers) and the per-stage
-    kernels (CUDA graph) run the same reductions in the same order: states,
-    step sequence and counters must agree bit for bit, rejections included."""
+def test_resident_kernel_matches_stage_kernels(model):
+    """The resident kernel (state in shared memory, grid all-reduce per
+    stage, control replicated in every block) and the stage kernels (CUDA
+    graphs) take the same adaptive step sequence, rejections included, and
+    agree to rounding (their reduction trees differ: 148 vs 296 partials)."""
     base = {"sa": "configs0", "bulb": "configs0", "ebulb": "configs0", "plane": "configs3",
             "cylinder": "configs4"}[model]
     cfg = baseline_config(base, Abins=24, Ebins=20, Ts=40, dr=0.5, max_dr=0.5, eps0=1e-9)
@@ -426,19 +427,17 @@ def test_persistent_kernel_bit_identical_to_stage_kernels(model):
     if base != "configs0":
         cfg.override("Pbins=8")
     out = []
-    for on in (True, False):
+    for mode in (Engine.LAUNCH_RESIDENT, Engine.LAUNCH_STAGES):
         env, eng = make(cfg)
-        try:
-            eng.set_launch_mode(Engine.LAUNCH_PERSISTENT if on else Engine.LAUNCH_STAGES)
-        except ConfigError:
-            pytest.skip("persistent kernel unavailable on this device")
+        eng.set_launch_mode(mode)
         n0 = eng.launch_count()
         s = eng.run(StepControl.from_config(cfg))
         out.append((s.iterations, s.accepted, s.rejected, s.final_r, eng.state(), eng.launch_count() - n0))
     (ia, aa, ra, fa, sa_, la), (ib, ab, rb, fb, sb, lb) = out
-    assert (ia, aa, ra, fa) == (ib, ab, rb, fb)
+    assert (ia, aa, ra) == (ib, ab, rb) and fa == pytest.approx(fb, rel=1e-13)
     assert ia == 40 and ra > 0
-    assert np.array_equal(sa_, sb)
+    (rg, _), (rw, _) = density(sa_, 20), density(sb, 20)
+    assert np.max(np.abs(rg - rw)) <= 1e-12
     assert la < lb  # one launch per batch instead of three per step
 
 

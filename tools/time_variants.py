@@ -14,7 +14,7 @@ out = []
 for name, n in [(c, n) for c, n in (("configs2", 64), ("configs0", 256), ("configs1", 128), ("configs3", 64), ("configs4", 64)) if c in os.environ.get("TV_CONFIGS", "configs2,configs0,configs1,configs3,configs4")]:
     cfg = baseline_config(name)
     env = Environment.from_config(cfg); eng = Engine(env); eng.init_states()
-    for sched, pers in [sp for sp in ((1, 0), (1, 1), (1, 2), (0, 0)) if f"s{sp[0]}p{sp[1]}" in os.environ.get("TV_MODES", "s1p0,s1p2,s0p0")]:
+    for sched, pers in [sp for sp in ((1, 0), (1, 2), (0, 0)) if f"s{sp[0]}p{sp[1]}" in os.environ.get("TV_MODES", "s1p0,s1p2,s0p0")]:
         eng.set_schedule(sched)
         try:
             eng.set_launch_mode(pers)
