@@ -150,6 +150,10 @@ struct DevBuf {
 
 using namespace oscb200;
 
+#ifndef OSC_GRAPH_STEPS
+#define OSC_GRAPH_STEPS 8  // steps per captured CUDA graph (stage kernels)
+#endif
+
 struct OscCtx {
     OscDesc desc{};
     int rank = 0, nranks = 1, device = 0;
@@ -303,8 +307,8 @@ struct OscCtx {
             launch_resident(n);
             return;
         }
-        if (n >= 8) {
-            if (!graph) build_graph(8);
+        if (n >= OSC_GRAPH_STEPS) {
+            if (!graph) build_graph(OSC_GRAPH_STEPS);
             for (; n >= graph_steps; n -= graph_steps) {
                 CUDA_OK(cudaGraphLaunch(graph, stream));
                 nlaunch += graph_kernels;
