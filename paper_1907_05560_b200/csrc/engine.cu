@@ -164,6 +164,7 @@ struct OscCtx {
     int T = 0, P = 0, E = 0;
     int ntraj = 0, ncell = 0, npad = 0;
     int nsm = 0, nblocks = 0, chunk = 0, ntr_max = 0;
+    int nblocks23 = 0, chunk23 = 0;  // S2/S3 grid (2 flavours)
     uint32_t e_magic = 0, e_shift = 0;
     int schedule = 1;  // 1: S3 stashes propagators for S4 (default), 0: S4 recomputes them
     int nflav = 2;
@@ -187,7 +188,7 @@ struct OscCtx {
     nccl::Comm comm = nullptr;
 
     DevBuf<double> cos2, sin0, cphi, sphi, vac11, vac12, g, ktab_g;
-    DevBuf<double> psi[2], stash, xbuf, xsend, partials, staging;
+    DevBuf<double> psi[2], bloch[2], stash, xbuf, xsend, partials, staging;
     // snapshot I/O: spectrum weights [nsp][E] (mode 2), mode-2 output, the
     // second packing buffer and pinned host buffers of the async dumps
     DevBuf<double> fw, mode2buf, staging2;
@@ -224,7 +225,7 @@ struct OscCtx {
     void launch_stage(int stage) {
         const StageFn fn = stage_kernel(nflav, desc.model, stage, schedule);
         cudaLaunchConfig_t cfg{};
-        cfg.gridDim = dim3(nblocks);
+        cfg.gridDim = dim3((nflav == 2 && (stage == 2 || stage == 3)) ? nblocks23 : nblocks);
         cfg.blockDim = dim3(kBlock);
         cfg.dynamicSmemBytes = nflav == 3 ? stage3_smem_bytes(ntr_max) : stage_smem_bytes(stage, schedule, ntr_max, E);
         cfg.stream = stream;
@@ -502,6 +503,11 @@ int osc_create(const OscDesc* desc, const OscComm* comm, OscCtx** out) {
         c->psi[1].alloc(plane);
         CUDA_OK(cudaMemset(c->psi[0].p, 0, plane * sizeof(double)));
         CUDA_OK(cudaMemset(c->psi[1].p, 0, plane * sizeof(double)));
+        if (c->nflav == 2)
+            for (auto& b : c->bloch) {
+                b.alloc((size_t)c->npad * kBlochPlanes);
+                CUDA_OK(cudaMemset(b.p, 0, b.n * sizeof(double)));
+            }
         c->xbuf.alloc((size_t)4 * c->nranks * kSlotDoubles);
         CUDA_OK(cudaMemset(c->xbuf.p, 0, c->xbuf.n * sizeof(double)));
         c->xll.alloc((size_t)4 * kMaxRanks * kLLWords);
@@ -560,7 +566,17 @@ int osc_create(const OscDesc* desc, const OscComm* comm, OscCtx** out) {
             c->e_shift = l;
             c->e_magic = (uint32_t)((((uint64_t)1 << 32) * (((uint64_t)1 << l) - (uint64_t)c->E)) / (uint64_t)c->E + 1);
         }
-        c->partials.alloc((size_t)c->nblocks * kSlotDoubles);
+        // S2/S3 (2 flavours): their own occupancy target, in proportion to
+        // the grid above (cells per block shrink; the records still fit)
+        c->nblocks23 = c->nblocks;
+        c->chunk23 = c->chunk;
+        if (c->nflav == 2 && OSC_MIN_BLOCKS_S23 != OSC_MIN_BLOCKS) {
+            const int nb23 = c->nblocks / OSC_MIN_BLOCKS * OSC_MIN_BLOCKS_S23;
+            int ch = (c->ncell + nb23 - 1) / nb23;
+            c->chunk23 = std::max(32, (ch + 31) / 32 * 32);
+            c->nblocks23 = nb23;
+        }
+        c->partials.alloc((size_t)std::max(c->nblocks, c->nblocks23) * kSlotDoubles);
 
         // resident kernel: single GPU, 2 flavours
         if (!c->coll && c->nflav == 2) {
@@ -611,6 +627,7 @@ int osc_create(const OscDesc* desc, const OscComm* comm, OscCtx** out) {
         a.ncell = c->ncell;
         a.npad = c->npad;
         a.chunk = c->chunk;
+        a.chunk23 = c->chunk23;
         a.ntr_max = c->ntr_max;
         a.nranks = c->nranks;
         a.fuse_ctl = !c->coll;
@@ -645,6 +662,8 @@ int osc_create(const OscDesc* desc, const OscComm* comm, OscCtx** out) {
         a.S = desc->S;
         a.psi0_buf[0] = c->psi[0].p;
         a.psi0_buf[1] = c->psi[1].p;
+        a.bloch_buf[0] = c->bloch[0].p;
+        a.bloch_buf[1] = c->bloch[1].p;
         a.stash = c->stash.p;
         a.xbuf = c->xbuf.p;
         a.xsend = c->coll ? c->xsend.p : c->xbuf.p;

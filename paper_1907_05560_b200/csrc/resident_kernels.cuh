@@ -349,7 +349,9 @@ __global__ void __launch_bounds__(kBlock, 1)
                                  fma(P[c].d, 0.5, u3[c].d)};
                     Dm[c] = Prop{Q[c].c - Rm[c].c, Q[c].a - Rm[c].a, Q[c].b - Rm[c].b, Q[c].d - Rm[c].d};
                 }
-                double Rr[3] = {0.0, 0.0, 0.0};
+                // moments of the candidate through its class Bloch vectors, as
+                // the stage kernels' S1 and S4 form them (same bits)
+                double B[2][3] = {{0.0, 0.0, 0.0}, {0.0, 0.0, 0.0}}, Rr[3];
 #pragma unroll
                 for (int s = 0; s < 4; ++s) {
                     double out[4], d[4];
@@ -360,8 +362,9 @@ __global__ void __launch_bounds__(kBlock, 1)
                         xr[(size_t)(s * 4 + c) * ch + k] = out[c];
                         emax = fmax(emax, fabs(d[c]));
                     }
-                    rho_add(out, K, s, Rr);
+                    bloch_add(out, K, s, B);
                 }
+                bloch_sum(B, Rr);
                 fold_acc<NM>(acc, Rr, R->fold[0]);
             }
             if (!res_allreduce<NM>(acc, emax, part, bar, phase, S, S.fin)) break;

@@ -437,7 +437,9 @@ def test_resident_kernel_matches_stage_kernels(model):
     assert (ia, aa, ra) == (ib, ab, rb) and fa == pytest.approx(fb, rel=1e-13)
     assert ia == 40 and ra > 0
     (rg, _), (rw, _) = density(sa_, 20), density(sb, 20)
-    assert np.max(np.abs(rg - rw)) <= 1e-12
+    # 40 unresolved adaptive steps (dr = 0.5 km) amplify the rounding of the
+    # two reduction trees to ~1e-12 (cylinder); the parity bar is 1e-8
+    assert np.max(np.abs(rg - rw)) <= 1e-11
     assert la < lb  # one launch per batch instead of three per step
 
 
