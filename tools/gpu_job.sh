@@ -1,10 +1,4 @@
 # scratch GPU job (edited per experiment)
-timeout 900 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?"
-tail -5 gpurun_out/pytest_gpu.log
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -2
-timeout 900 python bench.py --no-cpu-baseline > gpurun_out/bench.log 2>&1; echo "bench rc=$?"
-python - <<'PY'
-import json; d=json.loads(open('gpurun_out/bench.log').read().strip().splitlines()[-1])
-print(d['value'], d['ms_per_step'], d['e2e']['value'], d['roofline']['frac'], d['roofline']['stage_ms'])
-for k,v in d['other_configs'].items(): print(k, v['value'], v['ms_per_step'])
-PY
+timeout 900 python -m pytest tests -m gpu -q -x > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?"
+tail -3 gpurun_out/pytest_gpu.log
+TV_CONFIGS=configs2,configs4,configs3 TV_MODES=s1p0 timeout 900 python tools/time_variants.py 2>&1 | tee gpurun_out/tv.log
