@@ -250,6 +250,10 @@ int osc_fp64_peak(int device, double* dfma_per_s, double* ms);
 /* Average device time of each stage kernel (S2, S3, S4) over nsteps steps,
  * bracketed by CUDA events on the context stream (single-GPU contexts). */
 int osc_profile_stages(OscCtx* ctx, int nsteps, float* ms_out3);
+/* Development: per-block %globaltimer stamps of the stage launches of four
+ * iterations (layout in csrc/step_kernels.cuh, trace_mark); OSC_ERR_CONFIG
+ * unless the library was built with -DOSC_TRACE. */
+int osc_debug_trace(unsigned long long* out, size_t n);
 
 /* ---- host-side Environment builder (setup, not the hot path) ----------- */
 /* Mirrors solver::Environment::from_config (solver.cpp:62-95): angle grid,

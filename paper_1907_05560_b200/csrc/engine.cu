@@ -952,6 +952,20 @@ int osc_profile_stages(OscCtx* c, int nsteps, float* ms_out) {
     });
 }
 
+int osc_debug_trace(unsigned long long* out, size_t n) {
+    return guarded([&] {
+#if OSC_TRACE
+        const size_t have = (size_t)kTraceLaunches * kTraceBlocks * kTracePts;
+        CUDA_OK(cudaDeviceSynchronize());
+        CUDA_OK(cudaMemcpyFromSymbol(out, g_trace, std::min(n, have) * sizeof(unsigned long long)));
+#else
+        (void)out;
+        (void)n;
+        throw Error(OSC_ERR_CONFIG, "osc_debug_trace: library built without -DOSC_TRACE");
+#endif
+    });
+}
+
 int osc_max_norm_dev(OscCtx* c, double* out) {
     return guarded([&] {
         CUDA_OK(cudaSetDevice(c->device));
