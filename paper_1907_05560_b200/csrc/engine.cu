@@ -107,6 +107,15 @@ StageFn stage3_fn(int stage) {
         default: return k_stage3<MODEL, 4>;
     }
 }
+StageFn finalize_fn(int model) {
+    switch (model) {
+        case 0: return k_finalize<0>;
+        case 1: return k_finalize<1>;
+        case 2: return k_finalize<2>;
+        case 3: return k_finalize<3>;
+        default: return k_finalize<4>;
+    }
+}
 using ResidentFn = void (*)(StepArgs, int, int, int, double*, unsigned*);
 ResidentFn resident_kernel(int model) {
     switch (model) {
@@ -150,6 +159,12 @@ struct DevBuf {
 
 using namespace oscb200;
 
+#ifndef OSC_CR
+#define OSC_CR 1  // single GPU: consumer-side reduction of the stage partials (k_finalize per batch)
+#endif
+#ifndef OSC_GRID_WAVES
+#define OSC_GRID_WAVES 1  // waves of stage-kernel blocks (2: half-size chunks, SMs that finish early take more)
+#endif
 #ifndef OSC_GRAPH_STEPS
 #define OSC_GRAPH_STEPS 8  // steps per captured CUDA graph (stage kernels)
 #endif
@@ -188,6 +203,7 @@ struct OscCtx {
     nccl::Comm comm = nullptr;
 
     DevBuf<double> cos2, sin0, cphi, sphi, vac11, vac12, g, ktab_g;
+    DevBuf<double> cpart[4];  // single GPU: block partials of S2, S3, S4 (consumer-side reduction)
     DevBuf<double> psi[2], bloch[2], stash, xbuf, xsend, partials, staging;
     // snapshot I/O: spectrum weights [nsp][E] (mode 2), mode-2 output, the
     // second packing buffer and pinned host buffers of the async dumps
@@ -235,6 +251,23 @@ struct OscCtx {
         cfg.attrs = attr;
         cfg.numAttrs = 1;
         CUDA_OK(cudaLaunchKernelEx(&cfg, fn, args));
+        count();
+    }
+
+    // Single GPU: the control update of the last step of a batch (its S4
+    // partials are otherwise consumed by the next step's S2).
+    void finalize() {
+        if (!args.cr) return;
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(1);
+        cfg.blockDim = dim3(kBlock);
+        cfg.stream = stream;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = use_pdl ? 1 : 0;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        CUDA_OK(cudaLaunchKernelEx(&cfg, finalize_fn(desc.model), args));
         count();
     }
 
@@ -316,6 +349,7 @@ struct OscCtx {
             }
         }
         for (; n > 0; --n) enqueue_step();
+        finalize();
     }
 
     void download_ctl() {
@@ -358,6 +392,7 @@ struct OscCtx {
         h.err = 0.0;
         h.status = h.reason = 0;
         h.bad_sums = 0;
+        h.pend = 0;
         h.dump_mask = 0;  // snapshot gates are armed by osc_run_dumps only
         h.pause = 0;
         h.commit = commit;
@@ -531,7 +566,7 @@ int osc_create(const OscDesc* desc, const OscComm* comm, OscCtx** out) {
         // half-size chunks) instead of running at half occupancy.
         {
             const int occ = desc->nflav == 3 ? OSC3_MIN_BLOCKS : OSC_MIN_BLOCKS;
-            int nb = std::max(1, c->nsm * occ);
+            int nb = std::max(1, c->nsm * occ * (desc->nflav == 3 ? 1 : OSC_GRID_WAVES));
             for (int tries = 0;; ++tries) {
                 // 3 flavours: blocks split in halves by particle class
                 const int per = c->nflav == 3 ? nb / 2 : nb;
@@ -577,6 +612,11 @@ int osc_create(const OscDesc* desc, const OscComm* comm, OscCtx** out) {
             c->nblocks23 = nb23;
         }
         c->partials.alloc((size_t)std::max(c->nblocks, c->nblocks23) * kSlotDoubles);
+        if (!c->coll && c->nflav == 2)
+            for (int k = 1; k < 4; ++k) {
+                c->cpart[k].alloc((size_t)std::max(c->nblocks, c->nblocks23) * (2 * 12 + 1));
+                CUDA_OK(cudaMemset(c->cpart[k].p, 0, c->cpart[k].n * sizeof(double)));
+            }
 
         // resident kernel: single GPU, 2 flavours
         if (!c->coll && c->nflav == 2) {
@@ -631,6 +671,10 @@ int osc_create(const OscDesc* desc, const OscComm* comm, OscCtx** out) {
         a.ntr_max = c->ntr_max;
         a.nranks = c->nranks;
         a.fuse_ctl = !c->coll;
+        a.cr = (!c->coll && c->nflav == 2 && OSC_CR) ? 1 : 0;
+        a.nblocks = c->nblocks;
+        a.nblocks23 = c->nblocks23;
+        for (int k = 0; k < 4; ++k) a.cpart[k] = c->cpart[k].p;
         a.e_magic = c->e_magic;
         a.e_shift = c->e_shift;
         a.schedule = c->schedule;
@@ -757,6 +801,7 @@ int osc_trial_step_error(OscCtx* c, double r, double dr, double* err) {
         s.Rn = r + dr;
         c->begin(s, /*commit=*/0);
         c->enqueue_step();
+        c->finalize();
         c->download_ctl();
         c->raise_device_status();
         *err = c->h_ctl->err;
@@ -947,6 +992,8 @@ int osc_profile_stages(OscCtx* c, int nsteps, float* ms_out) {
                 acc[k] += ms;
             }
         }
+        c->finalize();
+        CUDA_OK(cudaStreamSynchronize(c->stream));
         for (auto& e : ev) cudaEventDestroy(e);
         for (int k = 0; k < 3; ++k) ms_out[k] = (float)(acc[k] / std::max(1, nsteps));
     });
