@@ -33,6 +33,8 @@ L, B, P = 12, 1024, 10
 buf = (C.c_ulonglong * (L * B * P))()
 assert lib().osc_debug_trace(buf, L * B * P) == 0
 t = np.frombuffer(buf, dtype=np.uint64).reshape(L, B, P).astype(np.float64)
+smid = t[:, :, 9].copy()
+t[:, :, 9] = 0
 nb = int((t[0, :, 0] > 0).sum())
 t = t[:, :nb]
 base = t[:, :, 0].min()
@@ -53,3 +55,25 @@ for l in range(L):
           f"{rel[:, 3].min():6.2f} {rel[:, 3].mean():6.2f} {rel[:, 3].max():6.2f}   {ex.mean():6.2f} {ex.max():6.2f}  "
           f"{rel[lb, 6]:6.2f} {rel[lb, 7]:6.2f} {rel[lb, 8]:6.2f} {done - prev_done:6.2f}")
     prev_done = done
+
+# per-block main-loop durations of the last traced S4 and S2: by SM and by block
+for l in (L - 1, L - 3):
+    x = t[l]
+    dur = x[:, 3] - x[:, 2]
+    sm = smid[l].astype(int)
+    order = np.argsort(dur)
+    print(f"{names[l % 3]} loop durations: min {dur.min():.2f} median {np.median(dur):.2f} max {dur.max():.2f} us")
+    print("  slowest blocks (block, sm, dur, start):", [(int(b), int(sm[b]), round(dur[b], 2), round(x[b, 2] - x[:, 2].min(), 2)) for b in order[-12:]])
+    print("  fastest blocks:", [(int(b), int(sm[b]), round(dur[b], 2)) for b in order[:6]])
+    # blocks sharing an SM: duration of the pair
+    per_sm = {}
+    for b in range(nb):
+        per_sm.setdefault(sm[b], []).append(dur[b])
+    sm_max = np.array([max(v) for v in per_sm.values()])
+    print(f"  per-SM max duration: min {sm_max.min():.2f} median {np.median(sm_max):.2f} max {sm_max.max():.2f}; SMs used {len(per_sm)}")
+    # correlation with block index (memory position)
+    q = np.array_split(np.arange(nb), 8)
+    print("  mean duration by block-index octile:", [round(float(dur[i].mean()), 2) for i in q])
+    sm = sm[:nb]
+    print("  mean duration by SM-id group of 18:",
+          [round(float(dur[sm // 18 == g].mean()), 2) for g in range(int(sm.max()) // 18 + 1) if (sm // 18 == g).any()])
