@@ -162,6 +162,9 @@ using namespace oscb200;
 #ifndef OSC_CR
 #define OSC_CR 1  // single GPU: consumer-side reduction of the stage partials (k_finalize per batch)
 #endif
+#ifndef OSC_EARLY_PDL
+#define OSC_EARLY_PDL 1  // one-wave grids release the next stage at their main loop's start
+#endif
 #ifndef OSC_GRID_WAVES
 #define OSC_GRID_WAVES 1  // waves of stage-kernel blocks (2: half-size chunks, SMs that finish early take more)
 #endif
@@ -180,6 +183,7 @@ struct OscCtx {
     int ntraj = 0, ncell = 0, npad = 0;
     int nsm = 0, nblocks = 0, chunk = 0, ntr_max = 0;
     int nblocks23 = 0, chunk23 = 0;  // S2/S3 grid (2 flavours)
+    int one_wave = 0;                // all stage grids resident at once (early programmatic launch)
     uint32_t e_magic = 0, e_shift = 0;
     int schedule = 1;  // 1: S3 stashes propagators for S4 (default), 0: S4 recomputes them
     int nflav = 2;
@@ -612,6 +616,20 @@ int osc_create(const OscDesc* desc, const OscComm* comm, OscCtx** out) {
             c->nblocks23 = nb23;
         }
         c->partials.alloc((size_t)std::max(c->nblocks, c->nblocks23) * kSlotDoubles);
+        // early dependent launch needs every stage grid resident at once
+        if (c->nflav == 2 && OSC_EARLY_PDL) {
+            int ok = 1;
+            for (int st : {0, 2, 3, 4})
+                for (int sch : {0, 1}) {
+                    int per = 0;
+                    const size_t sm = stage_smem_bytes(st, sch, c->ntr_max, c->E);
+                    CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, stage_kernel(2, desc->model, st, sch),
+                                                                          kBlock, sm));
+                    const int nb = (st == 2 || st == 3) ? c->nblocks23 : c->nblocks;
+                    if ((long long)per * c->nsm < nb) ok = 0;
+                }
+            c->one_wave = ok;
+        }
         if (!c->coll && c->nflav == 2)
             for (int k = 1; k < 4; ++k) {
                 c->cpart[k].alloc((size_t)std::max(c->nblocks, c->nblocks23) * (2 * 12 + 1));
@@ -674,6 +692,7 @@ int osc_create(const OscDesc* desc, const OscComm* comm, OscCtx** out) {
         a.cr = (!c->coll && c->nflav == 2 && OSC_CR) ? 1 : 0;
         a.nblocks = c->nblocks;
         a.nblocks23 = c->nblocks23;
+        a.one_wave = c->one_wave;
         for (int k = 0; k < 4; ++k) a.cpart[k] = c->cpart[k].p;
         a.e_magic = c->e_magic;
         a.e_shift = c->e_shift;

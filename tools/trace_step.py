@@ -53,7 +53,9 @@ for l in range(L):
     print(f"{l // 3}:{names[l % 3]}  {ent.min():6.2f} {ent.mean():6.2f} {ent.max():6.2f}   "
           f"{rel[:, 1].mean():6.2f} {rel[:, 1].max():6.2f}   {rel[:, 2].mean():6.2f} {rel[:, 2].max():6.2f}   "
           f"{rel[:, 3].min():6.2f} {rel[:, 3].mean():6.2f} {rel[:, 3].max():6.2f}   {ex.mean():6.2f} {ex.max():6.2f}  "
-          f"{rel[lb, 6]:6.2f} {rel[lb, 7]:6.2f} {rel[lb, 8]:6.2f} {done - prev_done:6.2f}")
+          f"{rel[lb, 6]:6.2f} {rel[lb, 7]:6.2f} {rel[lb, 8]:6.2f} {done - prev_done:6.2f}"
+          + ("" if not (x[:, 6] > 0).all() else
+             f"   [cr: waited {rel[:, 6].mean():6.2f} totals {rel[:, 7].mean():6.2f} ktab {rel[:, 8].mean():6.2f}]"))
     prev_done = done
 
 # per-block main-loop durations of the last traced S4 and S2: by SM and by block
