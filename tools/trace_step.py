@@ -29,7 +29,7 @@ ctl.Rn, ctl.Ts = 1e9, 0
 eng.begin(ctl)
 eng.enqueue_steps(32)
 eng.synchronize()
-L, B, P = 12, 1024, 10
+L, B, P = 12, 1024, 14
 buf = (C.c_ulonglong * (L * B * P))()
 assert lib().osc_debug_trace(buf, L * B * P) == 0
 t = np.frombuffer(buf, dtype=np.uint64).reshape(L, B, P).astype(np.float64)
@@ -55,7 +55,9 @@ for l in range(L):
           f"{rel[:, 3].min():6.2f} {rel[:, 3].mean():6.2f} {rel[:, 3].max():6.2f}   {ex.mean():6.2f} {ex.max():6.2f}  "
           f"{rel[lb, 6]:6.2f} {rel[lb, 7]:6.2f} {rel[lb, 8]:6.2f} {done - prev_done:6.2f}"
           + ("" if not (x[:, 6] > 0).all() else
-             f"   [cr: waited {rel[:, 6].mean():6.2f} totals {rel[:, 7].mean():6.2f} ktab {rel[:, 8].mean():6.2f}]"))
+             f"   [cr: waited {rel[:, 6].mean():6.2f} totals {rel[:, 7].mean():6.2f} ktab {rel[:, 8].mean():6.2f}]")
+          + ("" if not (x[:, 10] > 0).all() else
+             f"   [S2: wait done {rel[:, 10].mean():6.2f} reduced {rel[:, 11].mean():6.2f} decided {rel[:, 12].mean():6.2f}]"))
     prev_done = done
 
 # per-block main-loop durations of the last traced S4 and S2: by SM and by block
