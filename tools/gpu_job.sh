@@ -1,3 +1,3 @@
 # scratch GPU job (edited per experiment)
-timeout 900 python -m pytest tests -m gpu -q -x --timeout=120 > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?"; tail -3 gpurun_out/pytest_gpu.log
-timeout 300 python bench.py --no-cpu-baseline --no-other-configs > gpurun_out/bench.log 2>&1; echo "bench rc=$?"
+TV_CONFIGS=configs2,configs4,configs3 TV_MODES=s1p0,s0p0 timeout 400 python tools/time_variants.py 2>&1 | tee gpurun_out/tv.log
+timeout 600 python -m pytest tests -m gpu -q -x --timeout=120 > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?"; tail -3 gpurun_out/pytest_gpu.log
