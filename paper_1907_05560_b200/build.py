@@ -15,7 +15,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "_oscb200.so")
 SOURCES = ["engine.cu", "env.cpp"]
-HEADERS = ["step_kernels.cuh", "status.hpp"]
+HEADERS = ["step_kernels.cuh", "step3_kernels.cuh", "resident_kernels.cuh", "su3_exp.cuh", "fastmath.cuh", "status.hpp"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-shared", "-Xcompiler", "-fPIC,-O3",
