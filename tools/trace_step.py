@@ -57,7 +57,8 @@ for l in range(L):
           + ("" if not (x[:, 6] > 0).all() else
              f"   [cr: waited {rel[:, 6].mean():6.2f} totals {rel[:, 7].mean():6.2f} ktab {rel[:, 8].mean():6.2f}]")
           + ("" if not (x[:, 10] > 0).all() else
-             f"   [S2: wait done {rel[:, 10].mean():6.2f} reduced {rel[:, 11].mean():6.2f} decided {rel[:, 12].mean():6.2f}]"))
+             f"   [S2: wait done {rel[:, 10].mean():6.2f} reduced {rel[:, 11].mean():6.2f} decided {rel[:, 12].mean():6.2f}"
+             f" tma issued {rel[:, 13].mean():6.2f}]"))
     prev_done = done
 
 # per-block main-loop durations of the last traced S4 and S2: by SM and by block
