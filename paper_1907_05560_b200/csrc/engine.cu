@@ -184,6 +184,7 @@ struct OscCtx {
     int nsm = 0, nblocks = 0, chunk = 0, ntr_max = 0;
     int nblocks23 = 0, chunk23 = 0;  // S2/S3 grid (2 flavours)
     int one_wave = 0;                // all stage grids resident at once (early programmatic launch)
+    int rec_stride = 0;              // trajectory record stride (0: compact)
     uint32_t e_magic = 0, e_shift = 0;
     int schedule = 1;  // 1: S3 stashes propagators for S4 (default), 0: S4 recomputes them
     int nflav = 2;
@@ -247,7 +248,7 @@ struct OscCtx {
         cudaLaunchConfig_t cfg{};
         cfg.gridDim = dim3((nflav == 2 && (stage == 2 || stage == 3)) ? nblocks23 : nblocks);
         cfg.blockDim = dim3(kBlock);
-        cfg.dynamicSmemBytes = nflav == 3 ? stage3_smem_bytes(ntr_max) : stage_smem_bytes(stage, schedule, ntr_max, E);
+        cfg.dynamicSmemBytes = nflav == 3 ? stage3_smem_bytes(ntr_max) : stage_smem_bytes(stage, schedule, ntr_max, E, rec_stride);
         cfg.stream = stream;
         cudaLaunchAttribute attr[1];
         attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -583,8 +584,21 @@ int osc_create(const OscDesc* desc, const OscComm* comm, OscCtx** out) {
                 if (c->nflav == 3) {
                     smax = stage3_smem_bytes(c->ntr_max);
                 } else {
-                    for (int st : {0, 2, 3, 4})
-                        for (int sch : {0, 1}) smax = std::max(smax, stage_smem_bytes(st, sch, c->ntr_max, c->E));
+                    // padded record stride where two blocks per SM still fit, else compact
+                    for (int stride : {kRecStridePadded, 0}) {
+                        smax = 0;
+                        for (int st : {0, 2, 3, 4})
+                            for (int sch : {0, 1})
+                                smax = std::max(smax, stage_smem_bytes(st, sch, c->ntr_max, c->E, stride));
+                        c->rec_stride = stride;
+                        int per_sm = 0;
+                        CUDA_OK(cudaFuncSetAttribute(stage_kernel(2, desc->model, 4, 1),
+                                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                     (int)std::min<size_t>(smax, 227 * 1024)));
+                        CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+                            &per_sm, stage_kernel(2, desc->model, 4, 1), kBlock, std::min<size_t>(smax, 227 * 1024)));
+                        if (per_sm >= occ) break;
+                    }
                 }
                 if (smax > 200 * 1024)
                     throw Error(OSC_ERR_CONFIG, "osc_create: trajectory records exceed shared memory");
@@ -622,7 +636,7 @@ int osc_create(const OscDesc* desc, const OscComm* comm, OscCtx** out) {
             for (int st : {0, 2, 3, 4})
                 for (int sch : {0, 1}) {
                     int per = 0;
-                    const size_t sm = stage_smem_bytes(st, sch, c->ntr_max, c->E);
+                    const size_t sm = stage_smem_bytes(st, sch, c->ntr_max, c->E, c->rec_stride);
                     CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, stage_kernel(2, desc->model, st, sch),
                                                                           kBlock, sm));
                     const int nb = (st == 2 || st == 3) ? c->nblocks23 : c->nblocks;
@@ -693,6 +707,7 @@ int osc_create(const OscDesc* desc, const OscComm* comm, OscCtx** out) {
         a.nblocks = c->nblocks;
         a.nblocks23 = c->nblocks23;
         a.one_wave = c->one_wave;
+        a.rec_stride = c->rec_stride;
         for (int k = 0; k < 4; ++k) a.cpart[k] = c->cpart[k].p;
         a.e_magic = c->e_magic;
         a.e_shift = c->e_shift;
