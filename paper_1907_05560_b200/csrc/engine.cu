@@ -644,6 +644,11 @@ int osc_create(const OscDesc* desc, const OscComm* comm, OscCtx** out) {
                 }
             c->one_wave = ok;
         }
+        if (!c->coll && c->nflav == 3 && OSC_CR)
+            for (int k = 1; k < 3; ++k) {
+                c->cpart[k].alloc((size_t)c->nblocks * (2 * kNM3Max + 1));
+                CUDA_OK(cudaMemset(c->cpart[k].p, 0, c->cpart[k].n * sizeof(double)));
+            }
         if (!c->coll && c->nflav == 2)
             for (int k = 1; k < 4; ++k) {
                 c->cpart[k].alloc((size_t)std::max(c->nblocks, c->nblocks23) * (2 * 12 + 1));
@@ -704,6 +709,7 @@ int osc_create(const OscDesc* desc, const OscComm* comm, OscCtx** out) {
         a.nranks = c->nranks;
         a.fuse_ctl = !c->coll;
         a.cr = (!c->coll && c->nflav == 2 && OSC_CR) ? 1 : 0;
+        a.cr3 = (!c->coll && c->nflav == 3 && OSC_CR) ? 1 : 0;
         a.nblocks = c->nblocks;
         a.nblocks23 = c->nblocks23;
         a.one_wave = c->one_wave;

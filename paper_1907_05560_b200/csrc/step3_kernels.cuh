@@ -114,7 +114,32 @@ __global__ void __launch_bounds__(kBlock, OSC3_MIN_BLOCKS) k_stage3(StepArgs a) 
     const size_t np = a.npad;
     TrajRec3* rec = reinterpret_cast<TrajRec3*>(dsm3);
 
-    if (tid < 4 * NM) {
+    if (a.cr3 && (STAGE == 3 || STAGE == 4)) {
+        // single GPU: S2's / S3's block partials reduced here (the same tree
+        // their last block applied; cr_reduce, step_kernels.cuh), sums0 and
+        // (S4) sums1 | sums2 as S3's block 0 stored them
+        const double x0 = tid < NM ? __ldcg(a.xbuf + tid) : 0.0;
+        const double x1 = (STAGE == 4 && tid < 2 * NM)
+                              ? __ldcg(a.xbuf + kSlotDoubles + (tid < NM ? tid : 36 + tid - NM))
+                              : 0.0;
+        __shared__ double cfin[2 * kNM3Max + 1];
+        if (STAGE == 3)
+            cr_reduce<2 * NM>(a.cpart[1], (int)gridDim.x, red, cfin);
+        else
+            cr_reduce<NM>(a.cpart[2], (int)gridDim.x, red, cfin);
+        if (tid < NM) tot[0][tid] = x0;
+        if (STAGE == 4 && tid < 2 * NM) tot[1 + tid / NM][tid % NM] = x1;
+        if (tid < (STAGE == 3 ? 2 * NM : NM)) {
+            const int set = tid / NM, j = tid % NM;
+            const double v = cfin[set * NM + j];
+            tot[STAGE == 3 ? 1 + set : 3][j] = v;
+            if (blockIdx.x == 0) {
+                // slot layout: 36 doubles per set (S2: sums1 | sums2)
+                a.xbuf[(STAGE == 3 ? 1 : 2) * kSlotDoubles + set * 36 + j] = v;
+                if (!isfinite(v)) atomicOr(&a.ctl->bad_sums, 1);  // check_sums_finite
+            }
+        }
+    } else if (tid < 4 * NM) {
         const int h = tid / NM, k = tid % NM;
         if (Tr::hmask & (1 << h)) {
             const int slot = h == 0 ? 0 : (h == 3 ? 2 : 1);
@@ -292,6 +317,15 @@ __global__ void __launch_bounds__(kBlock, OSC3_MIN_BLOCKS) k_stage3(StepArgs a) 
     grid_launch_dependents();
 
     block_reduce<NV>(acc, emax, red);
+    if (a.cr3 && (STAGE == 2 || STAGE == 3)) {  // reduced by every block of S3 / S4
+        if (tid == 0) {
+            double* p = a.cpart[Tr::slot] + blockIdx.x;
+#pragma unroll
+            for (int k = 0; k < NV; ++k) p[(size_t)k * gridDim.x] = acc[k];
+            p[(size_t)NV * gridDim.x] = emax;
+        }
+        return;
+    }
     if (tid == 0) {
         // partials are stored [value][block]: the last block's loads of one
         // value across blocks coalesce (one request per 32 blocks)

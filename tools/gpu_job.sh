@@ -1,7 +1,3 @@
-# measurement: tests, smoke, bench (+ reference arm), launch list, full ncu capture
-timeout 900 python -m pytest tests -m gpu -q --timeout=120 > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?"; tail -2 gpurun_out/pytest_gpu.log
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?"
-timeout 900 python bench.py > gpurun_out/bench.log 2>&1; echo "bench rc=$?"
-timeout 900 python bench.py --impl reference > gpurun_out/bench_ref.log 2>&1; echo "bench ref rc=$?"
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-other-configs > gpurun_out/ncu_launch.log 2>&1; echo "ncu launch rc=$?"
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_stage -s 3 -c 3 -o gpurun_out/step_full5 python tools/profile_step.py --schedule 1 --steps 2 > gpurun_out/ncu_full.log 2>&1; echo "ncu full rc=$?"
+# scratch GPU job (edited per experiment)
+timeout 600 python -m pytest tests -m gpu -q -x --timeout=120 > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?"; tail -3 gpurun_out/pytest_gpu.log
+TV_CONFIGS=configs1 TV_MODES=s1p0 timeout 400 python tools/time_variants.py 2>&1 | tee gpurun_out/tv.log
