@@ -262,7 +262,7 @@ struct OscCtx {
     // Single GPU: the control update of the last step of a batch (its S4
     // partials are otherwise consumed by the next step's S2).
     void finalize() {
-        if (!args.cr) return;
+        if (!args.cr && !args.cr3) return;
         cudaLaunchConfig_t cfg{};
         cfg.gridDim = dim3(1);
         cfg.blockDim = dim3(kBlock);
@@ -272,7 +272,9 @@ struct OscCtx {
         attr[0].val.programmaticStreamSerializationAllowed = use_pdl ? 1 : 0;
         cfg.attrs = attr;
         cfg.numAttrs = 1;
-        CUDA_OK(cudaLaunchKernelEx(&cfg, finalize_fn(desc.model), args));
+        CUDA_OK(cudaLaunchKernelEx(&cfg, args.cr3 ? (desc.model == 0 ? k_finalize3<0> : k_finalize3<1>)
+                                                   : finalize_fn(desc.model),
+                                   args));
         count();
     }
 
@@ -645,7 +647,7 @@ int osc_create(const OscDesc* desc, const OscComm* comm, OscCtx** out) {
             c->one_wave = ok;
         }
         if (!c->coll && c->nflav == 3 && OSC_CR)
-            for (int k = 1; k < 3; ++k) {
+            for (int k = 1; k < 4; ++k) {
                 c->cpart[k].alloc((size_t)c->nblocks * (2 * kNM3Max + 1));
                 CUDA_OK(cudaMemset(c->cpart[k].p, 0, c->cpart[k].n * sizeof(double)));
             }

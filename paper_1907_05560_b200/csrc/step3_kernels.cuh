@@ -86,6 +86,67 @@ __device__ __forceinline__ void weighted_rho3(const double (&y)[3][6], const dou
     }
 }
 
+// Single GPU (a.cr3): lane_body's control for the previous step's S4 at the
+// start of S2 (and in k_finalize3), as cr_control does for 2 flavours: every
+// block reduces S4's block partials, decides on a shared copy of the control
+// block, block 0 stores it with the promoted sums0 and slot 3.  tot0: the
+// step's sums0 (NM values).
+template <int NM>
+__device__ __forceinline__ void cr_control3(const StepArgs& a, StageShared& S, bool finalize, double* tot0) {
+    const int tid = threadIdx.x;
+    for (int i = tid; i < kCtlWords; i += blockDim.x)
+        reinterpret_cast<unsigned long long*>(&S.cs)[i] = __ldcg(reinterpret_cast<const unsigned long long*>(a.ctl) + i);
+    const double x0 = tid < NM ? __ldcg(a.xbuf + tid) : 0.0;
+    cr_reduce<NM>(a.cpart[3], a.nblocks, S.red, S.fin);
+    Ctl& c = S.cs;
+    if (tid == 0) {
+        S.accept = c.pend ? ctl_advance(&c, a, S.fin[NM], c.bad_sums == 0) : -1;
+        S.r = c.r;
+        S.dr = c.dr;
+        S.A[0] = c.A[0];
+        S.A[1] = c.A[1];
+        S.A[2] = c.A[2];
+        S.iter = c.iter;
+        S.cur = c.cur;
+        S.stop = c.terminate | c.status | c.pause;
+        c.pend = (finalize || S.stop) ? 0 : 1;
+    }
+    __syncthreads();
+    if (tid < NM) {
+        const double v = S.accept == 1 ? S.fin[tid] : x0;
+        if (tot0) tot0[tid] = v;
+        if (blockIdx.x == 0) {
+            if (S.accept == 1) a.xbuf[tid] = v;
+            if (S.accept >= 0) {
+                a.xbuf[3 * kSlotDoubles + tid] = S.fin[tid];
+                if (tid == 0) a.xbuf[3 * kSlotDoubles + 36] = S.fin[NM];
+            }
+        }
+    }
+    if (blockIdx.x == 0 && tid == 0) {
+        Ctl* g = a.ctl;
+        __stcg(&g->err, c.err);
+        __stcg(&g->r, c.r);
+        __stcg(&g->dr, c.dr);
+        for (int k = 0; k < 3; ++k) __stcg(&g->A[k], c.A[k]);
+        __stcg(&g->iter, c.iter);
+        __stcg(&g->accepted, c.accepted);
+        __stcg(&g->rejected, c.rejected);
+        __stcg(&g->cur, c.cur);
+        __stcg(&g->terminate, c.terminate);
+        __stcg(&g->status, c.status);
+        __stcg(&g->reason, c.reason);
+        for (int m = 0; m < 2; ++m) {
+            __stcg(&g->mark_r[m], c.mark_r[m]);
+            __stcg(&g->mark_iter[m], c.mark_iter[m]);
+        }
+        __stcg(&g->pause, c.pause);
+        __stcg(&g->pend, c.pend);
+        __threadfence();
+    }
+    __syncthreads();
+}
+
 template <int MODEL, int STAGE>
 __global__ void __launch_bounds__(kBlock, OSC3_MIN_BLOCKS) k_stage3(StepArgs a) {
     using Tr = StageTraits<STAGE>;
@@ -99,16 +160,24 @@ __global__ void __launch_bounds__(kBlock, OSC3_MIN_BLOCKS) k_stage3(StepArgs a) 
 
     const Ctl* ctl = a.ctl;
     grid_dependency_wait();
-    if (STAGE != 0 && (ctl->terminate || ctl->status || ctl->pause)) return;
+    // S2 (single GPU): the previous step's control first (cr_control3)
+    __shared__ StageShared CS;
+    const bool ctl2 = STAGE == 2 && a.cr3;
+    if (ctl2) {
+        cr_control3<NM>(a, CS, false, &tot[0][0]);
+        if (CS.stop) return;
+    } else if (STAGE != 0 && (ctl->terminate || ctl->status || ctl->pause)) {
+        return;
+    }
     const int tid = threadIdx.x;
     const int nb_half = gridDim.x / 2;
     const int pc = blockIdx.x >= nb_half;
     const int hb_ = blockIdx.x - pc * nb_half;
     const int c0 = hb_ * a.chunk;
     const int c1 = min(c0 + a.chunk, a.ncell);
-    const double r = ctl->r, dr = ctl->dr;
+    const double r = ctl2 ? CS.r : ctl->r, dr = ctl2 ? CS.dr : ctl->dr;
     const double rk[3] = {r, r + 0.5 * dr, r + dr};
-    const int cur = ctl->cur;
+    const int cur = ctl2 ? CS.cur : ctl->cur;
     const double* __restrict__ psi0 = a.psi0_buf[cur];
     double* __restrict__ res = a.psi0_buf[cur ^ 1];
     const size_t np = a.npad;
@@ -139,7 +208,7 @@ __global__ void __launch_bounds__(kBlock, OSC3_MIN_BLOCKS) k_stage3(StepArgs a) 
                 if (!isfinite(v)) atomicOr(&a.ctl->bad_sums, 1);  // check_sums_finite
             }
         }
-    } else if (tid < 4 * NM) {
+    } else if (tid < 4 * NM && !ctl2) {
         const int h = tid / NM, k = tid % NM;
         if (Tr::hmask & (1 << h)) {
             const int slot = h == 0 ? 0 : (h == 3 ? 2 : 1);
@@ -156,7 +225,8 @@ __global__ void __launch_bounds__(kBlock, OSC3_MIN_BLOCKS) k_stage3(StepArgs a) 
         a.ctl->A[2] = matter_potential(a, rk[2]);
     }
     __syncthreads();
-    const double Am[3] = {STAGE ? ctl->A[0] : 0.0, STAGE ? ctl->A[1] : 0.0, STAGE ? ctl->A[2] : 0.0};
+    const double Am[3] = {ctl2 ? CS.A[0] : (STAGE ? ctl->A[0] : 0.0), ctl2 ? CS.A[1] : (STAGE ? ctl->A[1] : 0.0),
+                          ctl2 ? CS.A[2] : (STAGE ? ctl->A[2] : 0.0)};
     const int tr0 = c1 > c0 ? (int)div_e(c0, a.e_magic, a.e_shift) : 0;
     const int ntr = c1 > c0 ? (int)div_e(c1 - 1, a.e_magic, a.e_shift) - tr0 + 1 : 0;
     for (int i = tid; i < ntr; i += kBlock) {
@@ -317,7 +387,7 @@ __global__ void __launch_bounds__(kBlock, OSC3_MIN_BLOCKS) k_stage3(StepArgs a) 
     grid_launch_dependents();
 
     block_reduce<NV>(acc, emax, red);
-    if (a.cr3 && (STAGE == 2 || STAGE == 3)) {  // reduced by every block of S3 / S4
+    if (a.cr3 && (STAGE == 2 || STAGE == 3 || STAGE == 4)) {  // reduced by every block of S3 / S4 / next S2
         if (tid == 0) {
             double* p = a.cpart[Tr::slot] + blockIdx.x;
 #pragma unroll
@@ -392,6 +462,14 @@ __global__ void __launch_bounds__(kBlock, OSC3_MIN_BLOCKS) k_stage3(StepArgs a) 
 }
 
 inline size_t stage3_smem_bytes(int ntr_max) { return (size_t)ntr_max * sizeof(TrajRec3); }
+
+// Single GPU: the control update of a batch's last step (one block).
+template <int MODEL>
+__global__ void __launch_bounds__(kBlock, 1) k_finalize3(StepArgs a) {
+    __shared__ StageShared S;
+    grid_dependency_wait();
+    cr_control3<MODEL == 0 ? 9 : 18>(a, S, true, nullptr);
+}
 
 // 3-flavour init: pure flavour f = s / 2 plus eps noise on the other two
 // flavours, splitmix64-seeded by the global beam index j*6 + s (generalises
