@@ -147,6 +147,11 @@ __device__ __forceinline__ void cr_control3(const StepArgs& a, StageShared& S, b
     __syncthreads();
 }
 
+#ifndef OSC3_S4_OOL
+#define OSC3_S4_OOL 1
+#endif
+__device__ __noinline__ Mat3 exp_herm3_ool(const Herm3& H, double tau) { return exp_herm3(H, tau); }
+
 template <int MODEL, int STAGE>
 __global__ void __launch_bounds__(kBlock, OSC3_MIN_BLOCKS) k_stage3(StepArgs a) {
     using Tr = StageTraits<STAGE>;
@@ -287,7 +292,12 @@ __global__ void __launch_bounds__(kBlock, OSC3_MIN_BLOCKS) k_stage3(StepArgs a) 
 #pragma unroll
         for (int k = 0; k < 9; ++k) v[k] = __ldg(a.vac3 + (size_t)e * 9 + k);
         double Rr[9];
-        auto prop = [&](int h, int slot) { return exp_herm3(herm_of(v, R.hb[h], pc), R.dl[slot]); };
+        // S4 evaluates the exponential five times: one out-of-line copy there
+        // (inlined, the stage misses the instruction cache a third of the time)
+        auto prop = [&](int h, int slot) {
+            return (STAGE == 4 && OSC3_S4_OOL) ? exp_herm3_ool(herm_of(v, R.hb[h], pc), R.dl[slot])
+                                               : exp_herm3(herm_of(v, R.hb[h], pc), R.dl[slot]);
+        };
 
         if (STAGE == 0) {
             weighted_rho3(x, g, pc, Rr);
