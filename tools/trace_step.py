@@ -79,6 +79,9 @@ for l in (L - 1, L - 3):
     # correlation with block index (memory position)
     q = np.array_split(np.arange(nb), 8)
     print("  mean duration by block-index octile:", [round(float(dur[i].mean()), 2) for i in q])
+    st0 = x[:, 2] - x[:, 2].min()
+    print("  mean loop start by octile:", [round(float(st0[i].mean()), 2) for i in q])
+    print("  mean loop end by octile:  ", [round(float((x[:, 3] - x[:, 2].min())[i].mean()), 2) for i in q])
     sm = sm[:nb]
     print("  mean duration by SM-id group of 18:",
           [round(float(dur[sm // 18 == g].mean()), 2) for g in range(int(sm.max()) // 18 + 1) if (sm // 18 == g).any()])
