@@ -587,7 +587,11 @@ int osc_create(const OscDesc* desc, const OscComm* comm, OscCtx** out) {
                     smax = stage3_smem_bytes(c->ntr_max);
                 } else {
                     // padded record stride where two blocks per SM still fit, else compact
+                    // (env OSC_REC_COMPACT=1 forces the compact stride: tests)
+                    const char* rc_env = std::getenv("OSC_REC_COMPACT");
+                    const bool force_compact = rc_env && std::atoi(rc_env) == 1;
                     for (int stride : {kRecStridePadded, 0}) {
+                        if (force_compact && stride) continue;
                         smax = 0;
                         for (int st : {0, 2, 3, 4})
                             for (int sch : {0, 1})

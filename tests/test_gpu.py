@@ -574,3 +574,28 @@ def test_reference_host_code_with_engine_replaced(golden, cases, name, tmp_path)
     want = golden[f"{name}/final_state"]
     assert got.shape == want.shape
     assert np.max(np.abs(got - want)) <= 1e-12
+
+
+@pytest.mark.parametrize("model", ["bulb", "ebulb", "plane", "cylinder"])
+def test_compact_record_stride_is_bit_identical(model, monkeypatch):
+    """The trajectory records are laid out at a 256-byte stride when two
+    blocks per SM fit, at the stages' compact record size otherwise (few
+    energy bins per trajectory: configs[4] at full size).  Both layouts hold
+    the same values: forcing the compact one on a small problem must give the
+    same bits over an adaptive run with rejections."""
+    base = {"bulb": "configs0", "ebulb": "configs0", "plane": "configs3", "cylinder": "configs4"}[model]
+    cfg = baseline_config(base, Abins=24, Ebins=20, Ts=30, dr=0.5, max_dr=0.5, eps0=1e-9)
+    if model == "ebulb":
+        cfg.override("model=ebulb").override("Pbins=8").override("perturb=1e-6")
+    if base != "configs0":
+        cfg.override("Pbins=8")
+    out = []
+    for compact in ("0", "1"):
+        monkeypatch.setenv("OSC_REC_COMPACT", compact)
+        env, eng = make(cfg)
+        eng.set_launch_mode(Engine.LAUNCH_STAGES)
+        s = eng.run(StepControl.from_config(cfg))
+        out.append((s.iterations, s.accepted, s.rejected, eng.state()))
+    (ia, aa, ra, sa_), (ib, ab, rb, sb) = out
+    assert (ia, aa, ra) == (ib, ab, rb) and ra > 0
+    assert np.array_equal(sa_, sb)
