@@ -599,3 +599,29 @@ def test_compact_record_stride_is_bit_identical(model, monkeypatch):
     (ia, aa, ra, sa_), (ib, ab, rb, sb) = out
     assert (ia, aa, ra) == (ib, ab, rb) and ra > 0
     assert np.array_equal(sa_, sb)
+
+
+def test_batched_enqueue_matches_one_run():
+    """begin + enqueue_steps in uneven batches (partial graphs, a k_finalize
+    closing each batch, the next batch's S2 finding no pending result) ends
+    on the same bits, counters and radius as one run of the same length —
+    adaptive steps with rejections."""
+    cfg = baseline_config("configs0", Abins=24, Ebins=20, Ts=0, dr=0.5, max_dr=0.5, eps0=1e-9, Rn=1e9)
+    n_batches = (3, 5, 9, 1, 14)
+    env, eng = make(cfg)
+    eng.set_launch_mode(Engine.LAUNCH_STAGES)
+    eng.begin(StepControl.from_config(cfg))
+    for n in n_batches:
+        eng.enqueue_steps(n)
+        eng.synchronize()
+    q = eng.query()
+    a = eng.state()
+    ctl = StepControl.from_config(cfg)
+    ctl.Ts = sum(n_batches)
+    env2, eng2 = make(cfg)
+    eng2.set_launch_mode(Engine.LAUNCH_STAGES)
+    s = eng2.run(ctl)
+    assert q["status"] == 0 and q["iter"] == s.iterations == sum(n_batches)
+    assert q["accepted"] == s.accepted and q["rejected"] == s.rejected and s.rejected > 0
+    assert q["r"] == s.final_r
+    assert np.array_equal(a, eng2.state())
