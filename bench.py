@@ -377,7 +377,8 @@ def main():
         dist.destroy_process_group()
 
 
-LAUNCH_NAMES = {0: "stage kernels, PDL, CUDA graphs of 8 steps",
+LAUNCH_NAMES = {0: "stage kernels (PDL, one-wave early release, partials reduced by the next stage, "
+                   "control at the start of S2), CUDA graphs of 8 steps",
                 2: "resident kernel (state in shared memory, grid all-reduce per stage)"}
 
 
