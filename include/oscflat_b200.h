@@ -250,6 +250,13 @@ int osc_fp64_peak(int device, double* dfma_per_s, double* ms);
 /* Average device time of each stage kernel (S2, S3, S4) over nsteps steps,
  * bracketed by CUDA events on the context stream (single-GPU contexts). */
 int osc_profile_stages(OscCtx* ctx, int nsteps, float* ms_out3);
+/* flavor::evolve_bin (beam.hpp:105-121) through the device propagator code,
+ * for known-answer tests of its edge paths (lambda = 0, lambda dl < 1e-12,
+ * |lambda dl| > 1e9, subnormal lambda^2): h [n][3] (h11, h12_re, h12_im),
+ * dl [n], psi [n][4] (ar, ai, br, bi) -> out [n][4].  path 0: the stage
+ * kernels' branch-free chain with its fallback branch; 1: the safe path. */
+int osc_debug_evolve_bin(int device, size_t n, const double* h, const double* dl, const double* psi,
+                         double* out, int path);
 /* Development: per-block %globaltimer stamps of the stage launches of four
  * iterations (layout in csrc/step_kernels.cuh, trace_mark); OSC_ERR_CONFIG
  * unless the library was built with -DOSC_TRACE. */

@@ -159,6 +159,19 @@ struct DevBuf {
 
 using namespace oscb200;
 
+// The dynamic shared-memory limit is a per-kernel, process-wide attribute:
+// always set it to the most the kernel can take (the opt-in maximum less its
+// static shared memory), so a smaller context created later can never lower
+// it under a larger one's launches.
+template <class F>
+void set_max_dynamic_smem(F* fn, int device) {
+    int optin = 0;
+    CUDA_OK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
+    cudaFuncAttributes fa{};
+    CUDA_OK(cudaFuncGetAttributes(&fa, fn));
+    CUDA_OK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - (int)fa.sharedSizeBytes));
+}
+
 #ifndef OSC_CR
 #define OSC_CR 1  // single GPU: consumer-side reduction of the stage partials (k_finalize per batch)
 #endif
@@ -216,16 +229,31 @@ struct OscCtx {
     cudaStream_t copy_stream = nullptr;
     double* pinned[2] = {nullptr, nullptr};
     size_t pinned_n = 0;
+    // control block pair (StepArgs::ctl_out): `par` names the current one;
+    // single-GPU stage kernels flip it at every S2
     DevBuf<Ctl> ctl;
+    int par = 0;
+    Ctl* ctl_cur() const { return ctl.p + par; }
+    bool flips() const { return args.cr || args.cr3; }
     DevBuf<unsigned long long> scratch;
     Ctl* h_ctl = nullptr;  // pinned mirror
+    // the class Bloch planes of psi0 no longer match it (set_state, a
+    // resident batch): the stage kernels rerun S1 before their next step
+    bool bloch_stale = false;
 
     StepArgs args{};
-    cudaGraphExec_t graph = nullptr;
+    cudaGraphExec_t graph[2] = {nullptr, nullptr};  // by the control parity at launch
     int graph_steps = 0;
+    void drop_graphs() {
+        for (auto& g : graph)
+            if (g) {
+                cudaGraphExecDestroy(g);
+                g = nullptr;
+            }
+    }
 
     ~OscCtx() {
-        if (graph) cudaGraphExecDestroy(graph);
+        drop_graphs();
         if (comm) {
             try {
                 nccl::api().comm_destroy(comm);
@@ -245,6 +273,13 @@ struct OscCtx {
     // kernels orders the dependent reads).
     void launch_stage(int stage) {
         const StageFn fn = stage_kernel(nflav, desc.model, stage, schedule);
+        StepArgs la = args;  // (args.ctl == args.ctl_out == the current control block)
+        if (stage == 2 && flips()) {
+            // S2 reads the current control block and writes the advanced one
+            // into the other buffer, which becomes current
+            la.ctl_out = ctl.p + (par ^ 1);
+            set_par(par ^ 1);
+        }
         cudaLaunchConfig_t cfg{};
         cfg.gridDim = dim3((nflav == 2 && (stage == 2 || stage == 3)) ? nblocks23 : nblocks);
         cfg.blockDim = dim3(kBlock);
@@ -255,7 +290,7 @@ struct OscCtx {
         attr[0].val.programmaticStreamSerializationAllowed = use_pdl ? 1 : 0;
         cfg.attrs = attr;
         cfg.numAttrs = 1;
-        CUDA_OK(cudaLaunchKernelEx(&cfg, fn, args));
+        CUDA_OK(cudaLaunchKernelEx(&cfg, fn, la));
         count();
     }
 
@@ -307,11 +342,12 @@ struct OscCtx {
         exchange(0);
     }
 
-    void build_graph(int steps) {
-        if (graph) {
-            cudaGraphExecDestroy(graph);
-            graph = nullptr;
-        }
+    // A graph of `steps` (even) steps for the current control parity,
+    // instantiated and uploaded (so its first launch costs no setup).
+    cudaGraphExec_t get_graph(int steps) {
+        cudaGraphExec_t& gx = graph[par];
+        if (gx) return gx;
+        const int par0 = par;
         cudaGraph_t g_ = nullptr;
         CUDA_OK(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
         capturing = true;
@@ -319,9 +355,26 @@ struct OscCtx {
         for (int i = 0; i < steps; ++i) enqueue_step();
         capturing = false;
         CUDA_OK(cudaStreamEndCapture(stream, &g_));
-        CUDA_OK(cudaGraphInstantiate(&graph, g_, 0));
+        if (par != par0) throw Error(OSC_ERR_CUDA, "graph: odd number of control flips");
+        CUDA_OK(cudaGraphInstantiate(&gx, g_, 0));
         cudaGraphDestroy(g_);
+        CUDA_OK(cudaGraphUpload(gx, stream));
         graph_steps = steps;
+        return gx;
+    }
+    // Build (and upload) the step graphs of both parities now, outside any
+    // timed region.
+    void prepare_graphs() {
+        if (launch_mode != 0) return;
+        get_graph(OSC_GRAPH_STEPS);
+        if (!flips()) return;
+        set_par(par ^ 1);  // (host side only: nothing is launched)
+        get_graph(OSC_GRAPH_STEPS);
+        set_par(par ^ 1);
+    }
+    void set_par(int p) {
+        par = p;
+        args.ctl = args.ctl_out = ctl_cur();
     }
 
     // n steps in one cooperative launch with the state resident in shared
@@ -346,12 +399,17 @@ struct OscCtx {
         if (n <= 0) return;
         if (launch_mode == 2) {
             launch_resident(n);
+            bloch_stale = true;  // (the resident kernel keeps no Bloch planes)
             return;
         }
+        if (bloch_stale) {  // S1 rebuilds the Bloch planes (and sums0) of psi0
+            enqueue_moments0();
+            bloch_stale = false;
+        }
         if (n >= OSC_GRAPH_STEPS) {
-            if (!graph) build_graph(OSC_GRAPH_STEPS);
-            for (; n >= graph_steps; n -= graph_steps) {
-                CUDA_OK(cudaGraphLaunch(graph, stream));
+            cudaGraphExec_t gx = get_graph(OSC_GRAPH_STEPS);
+            for (; n >= OSC_GRAPH_STEPS; n -= OSC_GRAPH_STEPS) {
+                CUDA_OK(cudaGraphLaunch(gx, stream));
                 nlaunch += graph_kernels;
             }
         }
@@ -360,11 +418,11 @@ struct OscCtx {
     }
 
     void download_ctl() {
-        CUDA_OK(cudaMemcpyAsync(h_ctl, ctl.p, sizeof(Ctl), cudaMemcpyDeviceToHost, stream));
+        CUDA_OK(cudaMemcpyAsync(h_ctl, ctl_cur(), sizeof(Ctl), cudaMemcpyDeviceToHost, stream));
         CUDA_OK(cudaStreamSynchronize(stream));
     }
     void upload_ctl() {
-        CUDA_OK(cudaMemcpyAsync(ctl.p, h_ctl, sizeof(Ctl), cudaMemcpyHostToDevice, stream));
+        CUDA_OK(cudaMemcpyAsync(ctl_cur(), h_ctl, sizeof(Ctl), cudaMemcpyHostToDevice, stream));
         CUDA_OK(cudaStreamSynchronize(stream));
     }
 
@@ -420,6 +478,7 @@ struct OscCtx {
         if (!h.terminate) {
             check_radius(c.r);
             enqueue_moments0();
+            bloch_stale = false;
         }
     }
 };
@@ -439,6 +498,28 @@ __global__ void k_dfma_peak(double* out, int iters, double y, double z) {
 #pragma unroll
     for (int k = 0; k < 8; ++k) s += x[k];
     if (s == 12345.678) out[0] = s;  // keep the chains live
+}
+
+// flavor::evolve_bin (beam.hpp:105-121) through the production propagator
+// code: path 0 = make_props_n (branch-free chain, one fallback branch that
+// redoes the cell with the libdevice paths), 1 = the safe path only.  One
+// beam Hamiltonian per item: class 0 of CellK{v11 = v12 = 0} with hb = h.
+__global__ void k_debug_evolve(int n, const double* h, const double* dl, const double* psi, double* out, int path) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    CellK K{};
+    const double hb[3] = {h[3 * i], h[3 * i + 1], h[3 * i + 2]};
+    Prop u[2];
+    if (path == 0) {
+        const PropReq rq[1] = {{hb, dl[i], false, u}};
+        make_props_n(K, rq);
+    } else {
+        make_props_safe(K, hb, dl[i], false, u[0], u[1]);
+    }
+    const double x[4] = {psi[4 * i], psi[4 * i + 1], psi[4 * i + 2], psi[4 * i + 3]};
+    double y[4];
+    apply(u[0], x, y);
+    for (int k = 0; k < 4; ++k) out[4 * i + k] = y[k];
 }
 
 void validate(const OscDesc* d) {
@@ -558,8 +639,8 @@ int osc_create(const OscDesc* desc, const OscComm* comm, OscCtx** out) {
             c->xsend.alloc((size_t)4 * kSlotDoubles);
             CUDA_OK(cudaMemset(c->xsend.p, 0, c->xsend.n * sizeof(double)));
         }
-        c->ctl.alloc(1);
-        CUDA_OK(cudaMemset(c->ctl.p, 0, sizeof(Ctl)));
+        c->ctl.alloc(2);
+        CUDA_OK(cudaMemset(c->ctl.p, 0, 2 * sizeof(Ctl)));
         c->scratch.alloc(4);
         CUDA_OK(cudaMallocHost(&c->h_ctl, sizeof(Ctl)));
         std::memset(c->h_ctl, 0, sizeof(Ctl));
@@ -573,7 +654,9 @@ int osc_create(const OscDesc* desc, const OscComm* comm, OscCtx** out) {
         // half-size chunks) instead of running at half occupancy.
         {
             const int occ = desc->nflav == 3 ? OSC3_MIN_BLOCKS : OSC_MIN_BLOCKS;
-            int nb = std::max(1, c->nsm * occ * (desc->nflav == 3 ? 1 : OSC_GRID_WAVES));
+            int waves = OSC_GRID_WAVES;  // env OSC_GRID_WAVES overrides (tests: multi-wave grids)
+            if (const char* env = std::getenv("OSC_GRID_WAVES")) waves = std::max(1, std::atoi(env));
+            int nb = std::max(1, c->nsm * occ * (desc->nflav == 3 ? 1 : waves));
             for (int tries = 0;; ++tries) {
                 // 3 flavours: blocks split in halves by particle class
                 const int per = c->nflav == 3 ? nb / 2 : nb;
@@ -598,9 +681,7 @@ int osc_create(const OscDesc* desc, const OscComm* comm, OscCtx** out) {
                                 smax = std::max(smax, stage_smem_bytes(st, sch, c->ntr_max, c->E, stride));
                         c->rec_stride = stride;
                         int per_sm = 0;
-                        CUDA_OK(cudaFuncSetAttribute(stage_kernel(2, desc->model, 4, 1),
-                                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                     (int)std::min<size_t>(smax, 227 * 1024)));
+                        set_max_dynamic_smem(stage_kernel(2, desc->model, 4, 1), c->device);
                         CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
                             &per_sm, stage_kernel(2, desc->model, 4, 1), kBlock, std::min<size_t>(smax, 227 * 1024)));
                         if (per_sm >= occ) break;
@@ -609,9 +690,7 @@ int osc_create(const OscDesc* desc, const OscComm* comm, OscCtx** out) {
                 if (smax > 200 * 1024)
                     throw Error(OSC_ERR_CONFIG, "osc_create: trajectory records exceed shared memory");
                 for (int st : {0, 2, 3, 4})
-                    for (int sch : {0, 1})
-                        CUDA_OK(cudaFuncSetAttribute(stage_kernel(c->nflav, desc->model, st, sch),
-                                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smax));
+                    for (int sch : {0, 1}) set_max_dynamic_smem(stage_kernel(c->nflav, desc->model, st, sch), c->device);
                 if (c->nflav == 3 || tries >= 3 || chunk <= 32 * 32) break;
                 int per_sm = 0;
                 CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, stage_kernel(2, desc->model, 4, 1),
@@ -670,7 +749,7 @@ int osc_create(const OscDesc* desc, const OscComm* comm, OscCtx** out) {
             c->rsmem = resident_smem_bytes(c->rch, c->rntr, c->E);
             if (c->rsmem <= 200 * 1024 && OSC_DEBUG_MODE == 0) {
                 const ResidentFn rf = resident_kernel(desc->model);
-                CUDA_OK(cudaFuncSetAttribute(rf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->rsmem));
+                set_max_dynamic_smem(rf, c->device);
                 int rper = 0;
                 CUDA_OK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&rper, rf, kBlock, c->rsmem));
                 if (rper >= 1) {
@@ -761,7 +840,9 @@ int osc_create(const OscDesc* desc, const OscComm* comm, OscCtx** out) {
         a.rank = c->rank;
         a.xll = c->xll.p;
         a.partials = c->partials.p;
-        a.ctl = c->ctl.p;
+        a.ctl = a.ctl_out = c->ctl_cur();
+        a.ll_timeout_ns = 10000000000ll;  // 10 s
+        if (const char* env = std::getenv("OSC_LL_TIMEOUT_S")) a.ll_timeout_ns = (long long)(std::atof(env) * 1e9);
         CUDA_OK(cudaDeviceSynchronize());
         *out = c.release();
     });
@@ -806,6 +887,7 @@ static void set_state_impl(OscCtx* c, const double* src, size_t n, cudaMemcpyKin
     CUDA_OK(cudaMemcpyAsync(c->staging.p, src, want * sizeof(double), kind, c->stream));
     k_unpack<<<c->nsm * 8, 256, 0, c->stream>>>(c->args, c->staging.p, want); c->count();
     CUDA_OK(cudaGetLastError());
+    c->bloch_stale = true;
     CUDA_OK(cudaStreamSynchronize(c->stream));
 }
 
@@ -858,6 +940,7 @@ int osc_begin(OscCtx* c, const OscStepControl* ctl) {
     return guarded([&] {
         CUDA_OK(cudaSetDevice(c->device));
         c->begin(*ctl, 1);
+        c->prepare_graphs();
     });
 }
 
@@ -926,10 +1009,7 @@ int osc_set_schedule(OscCtx* c, int schedule) {
         c->schedule = schedule;
         c->args.schedule = schedule;
         c->args.stash = c->stash.p;
-        if (c->graph) {
-            cudaGraphExecDestroy(c->graph);
-            c->graph = nullptr;
-        }
+        c->drop_graphs();
     });
 }
 
@@ -978,10 +1058,7 @@ int osc_comm_connect(OscCtx* c, const void* handles) {
             a.peer_xll[q] = static_cast<unsigned long long*>(pb);
         }
         a.p2p = 1;
-        if (c->graph) {  // kernel arguments changed
-            cudaGraphExecDestroy(c->graph);
-            c->graph = nullptr;
-        }
+        c->drop_graphs();  // kernel arguments changed
     });
 }
 
@@ -1013,6 +1090,24 @@ int osc_fp64_peak(int device, double* dfma_per_s, double* ms_out) {
         cudaFree(d);
         *dfma_per_s = (double)blocks * threads * 8.0 * iters / (best * 1e-3);
         if (ms_out) *ms_out = best;
+    });
+}
+
+int osc_debug_evolve_bin(int device, size_t n, const double* h, const double* dl, const double* psi,
+                         double* out, int path) {
+    return guarded([&] {
+        if (n == 0) return;
+        if (!h || !dl || !psi || !out) throw Error(OSC_ERR_CONFIG, "osc_debug_evolve_bin: null argument");
+        CUDA_OK(cudaSetDevice(device));
+        double* d = nullptr;
+        CUDA_OK(cudaMalloc(&d, n * 12 * sizeof(double)));
+        std::unique_ptr<double, decltype(&cudaFree)> hold(d, &cudaFree);
+        CUDA_OK(cudaMemcpy(d, h, n * 3 * sizeof(double), cudaMemcpyHostToDevice));
+        CUDA_OK(cudaMemcpy(d + 3 * n, dl, n * sizeof(double), cudaMemcpyHostToDevice));
+        CUDA_OK(cudaMemcpy(d + 4 * n, psi, n * 4 * sizeof(double), cudaMemcpyHostToDevice));
+        k_debug_evolve<<<(unsigned)((n + 127) / 128), 128>>>((int)n, d, d + 3 * n, d + 4 * n, d + 8 * n, path);
+        CUDA_OK(cudaGetLastError());
+        CUDA_OK(cudaMemcpy(out, d + 8 * n, n * 4 * sizeof(double), cudaMemcpyDeviceToHost));
     });
 }
 
@@ -1235,7 +1330,7 @@ int osc_run_dumps(OscCtx* c, const OscStepControl* ctl, const OscDumpGates* gate
                     take_dump(m + 1, meta);
                 }
                 h.pause = 0;
-                CUDA_OK(cudaMemcpyAsync(c->ctl.p, c->h_ctl, sizeof(Ctl), cudaMemcpyHostToDevice, c->stream));
+                CUDA_OK(cudaMemcpyAsync(c->ctl_cur(), c->h_ctl, sizeof(Ctl), cudaMemcpyHostToDevice, c->stream));
             }
             if (!term && ctl->Tn > 0.0 && secs() >= ctl->Tn) term = 3;
             // keep the device busy while the host delivers finished dumps

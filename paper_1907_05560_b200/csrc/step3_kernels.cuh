@@ -123,27 +123,8 @@ __device__ __forceinline__ void cr_control3(const StepArgs& a, StageShared& S, b
             }
         }
     }
-    if (blockIdx.x == 0 && tid == 0) {
-        Ctl* g = a.ctl;
-        __stcg(&g->err, c.err);
-        __stcg(&g->r, c.r);
-        __stcg(&g->dr, c.dr);
-        for (int k = 0; k < 3; ++k) __stcg(&g->A[k], c.A[k]);
-        __stcg(&g->iter, c.iter);
-        __stcg(&g->accepted, c.accepted);
-        __stcg(&g->rejected, c.rejected);
-        __stcg(&g->cur, c.cur);
-        __stcg(&g->terminate, c.terminate);
-        __stcg(&g->status, c.status);
-        __stcg(&g->reason, c.reason);
-        for (int m = 0; m < 2; ++m) {
-            __stcg(&g->mark_r[m], c.mark_r[m]);
-            __stcg(&g->mark_iter[m], c.mark_iter[m]);
-        }
-        __stcg(&g->pause, c.pause);
-        __stcg(&g->pend, c.pend);
-        __threadfence();
-    }
+    // the advanced copy goes to the other control buffer (see StepArgs::ctl_out)
+    if (blockIdx.x == 0) store_ctl(a.ctl_out, c);
     __syncthreads();
 }
 

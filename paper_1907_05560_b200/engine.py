@@ -365,6 +365,23 @@ def fp64_peak(device: int = 0) -> float:
     return v.value
 
 
+def debug_evolve_bin(h, dl, psi, path: int = 0, device: int = 0):
+    """flavor::evolve_bin (beam.hpp:105-121) through the device propagator
+    code (path 0: the stage kernels' branch-free chain + fallback branch; 1:
+    the safe path).  h [n,3], dl [n], psi [n,4] -> [n,4]."""
+    import numpy as np
+
+    h = np.ascontiguousarray(h, dtype=np.float64).reshape(-1, 3)
+    n = h.shape[0]
+    dl = np.ascontiguousarray(dl, dtype=np.float64).reshape(n)
+    psi = np.ascontiguousarray(psi, dtype=np.float64).reshape(n, 4)
+    out = np.zeros((n, 4))
+    dp = C.POINTER(C.c_double)
+    check(lib().osc_debug_evolve_bin(device, n, h.ctypes.data_as(dp), dl.ctypes.data_as(dp),
+                                     psi.ctypes.data_as(dp), out.ctypes.data_as(dp), path))
+    return out
+
+
 def comm_unique_id() -> bytes:
     buf = C.create_string_buffer(128)
     check(lib().osc_comm_unique_id(buf))

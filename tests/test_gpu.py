@@ -113,15 +113,92 @@ def test_configs0_shape_resolved_window_vs_oracle(pyoracle):
     assert s.final_max_norm_dev <= TRACE_TOL
 
 
-def test_configs0_shape_vs_compiled_reference(ref):
-    """Same window, against the unmodified reference engine on all host cores."""
+@pytest.mark.parametrize("mode", ["resident", "stages"])
+def test_configs0_shape_vs_compiled_reference(ref, mode):
+    """Same window, against the unmodified reference engine on all host cores,
+    through both single-GPU launch paths (resident kernel: 148-block grid
+    all-reduce; stage kernels: 296-block consumer-side reduction)."""
     cfg = baseline_config("configs0", R0=50, Rn=60, dr=5e-5, max_dr=5e-5, Ts=100)
     env, eng = make(cfg)
-    eng.run(StepControl.from_config(cfg))
+    eng.set_launch_mode(Engine.LAUNCH_RESIDENT if mode == "resident" else Engine.LAUNCH_STAGES)
+    s = eng.run(StepControl.from_config(cfg))
     want, summ = ref.run(cfg.render(), lanes=min(os.cpu_count() or 1, 16))
-    (rg, _), (rw, _) = density(eng.state(), env.ebins), density(want, env.ebins)
-    assert summ["iterations"] == 100
+    (rg, tg), (rw, tw) = density(eng.state(), env.ebins), density(want, env.ebins)
+    assert summ["iterations"] == s.iterations == 100
     assert np.max(np.abs(rg - rw)) <= RHO_TOL
+    assert np.max(np.abs(tg - 1.0)) <= TRACE_TOL and np.max(np.abs(tw - 1.0)) <= TRACE_TOL
+
+
+def test_configs2_full_size_vs_compiled_reference(ref):
+    """The headline workload at full size (4096 x 256 = 1M beams, the stage
+    kernels' 296-block reduction tree) against the unmodified reference
+    engine in the resolved window: same iteration count,
+    every rho component within 1e-8, trace within 1e-12 on both sides."""
+    cfg = baseline_config("configs2", R0=50, Rn=60, dr=5e-5, max_dr=5e-5, Ts=20)
+    env, eng = make(cfg)
+    assert eng.launch_mode == Engine.LAUNCH_STAGES
+    s = eng.run(StepControl.from_config(cfg))
+    want, summ = ref.run(cfg.render(), lanes=min(os.cpu_count() or 1, 16))
+    assert summ["iterations"] == s.iterations == 20
+    assert s.final_r == pytest.approx(summ["final_r"], rel=1e-14)
+    (rg, tg), (rw, tw) = density(eng.state(), env.ebins), density(want, env.ebins)
+    assert np.max(np.abs(rg - rw)) <= RHO_TOL
+    assert np.max(np.abs(tg - 1.0)) <= TRACE_TOL and np.max(np.abs(tw - 1.0)) <= TRACE_TOL
+
+
+@pytest.mark.parametrize("name,kw", [
+    ("configs3", dict(R0=0.0, Rn=1.0, dr=1e-7, max_dr=1e-7, Ts=3)),  # (dr = 1e-6: trace drifts 1.6e-12 in the oracle too)
+    ("configs4", dict(R0=30.0, Rn=31.0, dr=1e-6, max_dr=1e-6, Ts=3)),
+])
+def test_plane_cylinder_full_size_vs_oracle(pyoracle, name, kw):
+    """configs[3] (256x64x64 plane, 1M beams) and configs[4] (512x128x32
+    cylinder, 2M beams) at full size: GPU vs the C restatement (parity
+    unpinned w.r.t. the reference, which has neither model)."""
+    cfg = baseline_config(name, **kw)
+    env, eng = make(cfg)
+    s = eng.run(StepControl.from_config(cfg))
+    o = pyoracle.Oracle(cfg)
+    so = o.run()
+    assert s.iterations == so["iterations"] == kw["Ts"]
+    (rg, tg), (ro, to) = density(eng.state(), env.ebins), density(o.get_state(), env.ebins)
+    assert np.max(np.abs(rg - ro)) <= RHO_TOL
+    assert np.max(np.abs(tg - 1.0)) <= TRACE_TOL
+
+
+def test_three_flavour_full_size_vs_oracle(pyoracle):
+    """configs[1] at full size (512 x 128, 3x3 rho) for a few resolved steps:
+    GPU (closed-form SU(3)) vs the C restatement (series exponential)."""
+    cfg = baseline_config("configs1", R0=50, Rn=51, dr=1e-6, max_dr=1e-6, Ts=3)
+    env, eng = make(cfg)
+    s = eng.run(StepControl.from_config(cfg))
+    o = pyoracle.Oracle3(cfg)
+    so = o.run()
+    assert s.iterations == so["iterations"] == 3
+    nt = env.abins * env.pbins
+    (rg, tg), (ro, _) = rho3(eng.state(), nt, env.ebins), rho3(o.get_state(), nt, env.ebins)
+    assert np.abs(rg - ro).max() <= RHO_TOL
+    assert np.abs(tg - 1.0).max() <= TRACE_TOL
+
+
+def test_multi_wave_grid_takes_the_same_steps(monkeypatch):
+    """Stage grids of two waves (OSC_GRID_WAVES=2: the second wave's blocks
+    start only after first-wave blocks retire) must take the same adaptive
+    step sequence as one-wave grids: every S2 block decides the previous
+    step's control from the same control block (double-buffered by step
+    parity), never from one another S2 block already advanced."""
+    cfg = baseline_config("configs0", Abins=96, Ebins=64, Ts=40, dr=0.5, max_dr=0.5, eps0=1e-9)
+    out = []
+    for waves in ("1", "2", "4"):
+        monkeypatch.setenv("OSC_GRID_WAVES", waves)
+        env, eng = make(cfg)
+        eng.set_launch_mode(Engine.LAUNCH_STAGES)
+        s = eng.run(StepControl.from_config(cfg))
+        out.append((s.iterations, s.accepted, s.rejected, s.final_r, eng.state()))
+    for it, acc, rej, fr, st in out[1:]:
+        assert (it, acc, rej) == out[0][:3] and rej > 0
+        assert fr == pytest.approx(out[0][3], rel=1e-13)
+        (rg, _), (rw, _) = density(st, 64), density(out[0][4], 64)
+        assert np.max(np.abs(rg - rw)) <= 1e-11
 
 
 def test_ebulb_symmetry_breaking_vs_oracle(pyoracle):
@@ -145,17 +222,18 @@ def test_full_size_configs2_properties():
     s0 = eng.state()
     eng.set_state(s0)
     assert np.array_equal(eng.state(), s0)  # mode-1 round trip
+    eng.set_schedule(0)  # S4 recomputes the half2 propagator
     s = eng.run(StepControl.from_config(cfg))
     a = eng.state()
     assert s.iterations == 20 and s.final_max_norm_dev <= TRACE_TOL
     eng.set_state(s0)
-    eng.set_schedule(1)  # stash half2 instead of recomputing it
+    eng.set_schedule(1)  # S3 stashes it for S4 (default)
     eng.run(StepControl.from_config(cfg))
-    assert np.array_equal(eng.state(), a)  # bitwise: same arithmetic, same order
+    b = eng.state()
+    assert np.array_equal(b, a)  # bitwise: same arithmetic, same order
     eng.set_state(s0)
-    eng.set_schedule(0)
     eng.run(StepControl.from_config(cfg))
-    assert np.array_equal(eng.state(), a)  # deterministic reductions
+    assert np.array_equal(eng.state(), b)  # deterministic reductions
     _, t = density(a, env.ebins)
     assert np.max(np.abs(t - 1.0)) <= TRACE_TOL
 
@@ -625,3 +703,38 @@ def test_batched_enqueue_matches_one_run():
     assert q["accepted"] == s.accepted and q["rejected"] == s.rejected and s.rejected > 0
     assert q["r"] == s.final_r
     assert np.array_equal(a, eng2.state())
+
+
+# ------------------------------- evolve_bin edge paths on the device (beam.hpp:105-121)
+def _evolve_tol(h, dl, psi):
+    """8 ulp of the amplitudes plus the phase conditioning of the step: a
+    one-ulp difference in lambda (sqrt vs l2*rsqrt, FMA contraction of l2)
+    moves the phase lambda*dl by |lambda dl| * 2^-53, which the reference's own
+    FMA and no-FMA builds show as well."""
+    ldl = np.linalg.norm(h, axis=1) * dl
+    return 8 * 2.0 ** -53 * np.maximum(1.0, np.abs(psi).max(axis=1)) + 4 * ldl * 2.0 ** -53
+
+
+@pytest.mark.parametrize("path", [0, 1])
+def test_evolve_bin_edge_paths_match_reference(path):
+    """lambda = 0, lambda*dl < 1e-12, |lambda*dl| > 1e9, subnormal lambda^2 and
+    lambda^2 > 1e300 through the stage kernels' propagator code (path 0: the
+    branch-free chain and its fallback branch; 1: the safe path alone) vs the
+    unmodified reference's evolve_bin (tests/golden/kat_edge.npz), plus the
+    reference KATs of golden.npz."""
+    from paper_1907_05560_b200.engine import debug_evolve_bin
+
+    d = np.load(os.path.join(GOLD, "kat_edge.npz"))
+    g = np.load(os.path.join(GOLD, "golden.npz"))
+    for h, dl, psi, want, tag in ((d["h"], d["dl"], d["psi"], d["evolve"], d["tag"]),
+                                  (g["kat_h"], g["kat_dl"], g["kat_psi"], g["kat_evolve"],
+                                   np.array(["golden"] * len(g["kat_dl"])))):
+        got = debug_evolve_bin(h, dl, psi, path=path)
+        err = np.abs(got - want).max(axis=1)
+        tol = _evolve_tol(h, dl, psi)
+        bad = np.nonzero(err > tol)[0]
+        assert bad.size == 0, [(tag[i], err[i], tol[i]) for i in bad[:5]]
+        # the limits themselves: identity for lambda = 0, unitarity everywhere
+        z = np.linalg.norm(h, axis=1) == 0.0
+        assert np.array_equal(got[z], psi[z])
+        assert np.abs(np.linalg.norm(got, axis=1) - np.linalg.norm(psi, axis=1)).max() <= 4e-16

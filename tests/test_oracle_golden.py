@@ -37,6 +37,19 @@ def test_evolve_bin_kats(pyoracle, golden):
         assert np.max(np.abs(got - want)) <= 4e-16 * 8
 
 
+def test_evolve_bin_edge_kats(pyoracle):
+    """The restatement's evolve_bin on the edge fixture the reference produced
+    (tests/golden/make_edge_kats.py): lambda = 0, lambda*dl < 1e-12 and just
+    above, |lambda*dl| > 1e9, subnormal and > 1e300 lambda^2."""
+    d = np.load(os.path.join(GOLD, "kat_edge.npz"))
+    o = pyoracle.Oracle(parse_config(json.load(open(os.path.join(GOLD, "golden_meta.json")))
+                                     ["cases"]["bulb_resolved"]))
+    for h, dl, psi, want in zip(d["h"], d["dl"], d["psi"], d["evolve"]):
+        got = o.evolve_bin(h, dl, psi)
+        tol = 8 * 2.0 ** -53 + 4 * np.linalg.norm(h) * dl * 2.0 ** -53
+        assert np.max(np.abs(got - want)) <= tol
+
+
 def test_init_state_bit_exact(pyoracle, golden):
     k = 0
     for s in range(4):
