@@ -97,6 +97,8 @@ typedef struct OscComm {
                                    one GPU) */
 } OscComm;
 #define OSC_COMM_FORCE_COLLECTIVES 1
+#define OSC_COMM_GROUP 2 /* (set by osc_create_group on its ranks: the group
+                            drives the exchange, no NCCL communicator) */
 
 /* solver::StepControl (solver.hpp:20-34) */
 typedef struct OscStepControl {
@@ -170,7 +172,32 @@ int osc_comm_connect(OscCtx* ctx, const void* handles);
 int osc_create(const OscDesc* desc, const OscComm* comm, OscCtx** out);
 int osc_destroy(OscCtx* ctx);
 
-/* Local theta block [t_lo, t_hi) and local state size in doubles. */
+/* Engine(env, lanes) in ONE process over several GPUs — the in-process
+ * counterpart of par::run_lanes (parallel.cpp:224-253): nranks contexts, rank
+ * q on devices[q] (NULL: q mod the device count) holding theta block q of
+ * make_partitions (parallel.cpp:11-24), driven by the calling thread through
+ * the returned group handle, which every entry point below accepts like a
+ * single context (state payloads then cover all trajectories, in order).
+ * Moment exchange between the stages:
+ *   - device-initiated (default when every rank has its own GPU and all pairs
+ *     have peer access): the last block of each stage stores its rank's slot
+ *     into every rank's buffer over NVLink through peer pointers (the
+ *     osc_comm_connect path without IPC), consumers poll sequence-flagged words;
+ *   - stream-ordered (OSC_GROUP_ORDERED, or forced by a shared GPU): the rank
+ *     slots are copied between the ranks' exchange buffers behind
+ *     cross-stream events after every stage, a control kernel per rank after
+ *     S4.  No kernel ever waits on another rank's kernel, so several ranks may
+ *     share one GPU (tests).
+ * nranks == 1 returns a plain context (osc_create with OscComm{0, 1, dev}). */
+#define OSC_GROUP_ORDERED 1
+int osc_create_group(const OscDesc* desc, int nranks, const int* devices, int flags, OscCtx** out);
+/* Ranks of a context (1 unless a group) and its exchange (1: stream-ordered). */
+int osc_group_info(const OscCtx* ctx, int* nranks, int* ordered);
+/* Visible CUDA devices (0 when none). */
+int osc_device_count(int* n);
+
+/* Local theta block [t_lo, t_hi) and local state size in doubles (a group:
+ * [0, abins) and the whole state). */
 int osc_local_range(const OscCtx* ctx, int* t_lo, int* t_hi, size_t* state_doubles);
 
 /* Engine::init_states — solver.cpp:475-478 / 255-271 (splitmix64 noise with

@@ -13,7 +13,9 @@
 // ParallelError from the C status codes.  One semantic change: state() is a
 // host copy of the device state (refreshed on each call; writes through it —
 // resume_from — are pushed before the next trial step or run).
+#include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <span>
@@ -24,6 +26,7 @@
 #include "oscflat/solver.hpp"
 #include "oscflat/types.hpp"
 #include "oscflat_b200.h"
+#include "solver_b200.hpp"
 
 namespace oscflat::solver {
 namespace {
@@ -43,6 +46,8 @@ void ok(int rc) {
 
 }  // namespace
 
+RunSummary summary_of(const OscRunSummary& s);
+
 struct Engine::Impl {
     const Environment* env;
     OscCtx* ctx = nullptr;
@@ -50,8 +55,15 @@ struct Engine::Impl {
     std::vector<double> payload;  // mode-1 staging
     bool host_dirty = false;      // state() handed out mutably since the last push
 
-    Impl(const Environment& e, int lanes) : env(&e), host(e.grid, e.ebins) {
+    int lanes = 1;
+    int gpus = 1;
+
+    Impl(const Environment& e, int lanes_) : env(&e), host(e.grid, e.ebins), lanes(lanes_) {
+        // the reference constructor's checks, same messages (solver.cpp:459-466)
         if (lanes < 1) throw ConfigError("Engine: lanes must be >= 1");
+        if (e.grid.model == geom::Model::SingleAngle && lanes != 1)
+            throw ConfigError("single-angle model does not support multiple workers");
+        if (lanes > e.grid.abins) throw ConfigError("Engine: more lanes than theta bins");
         std::vector<double> fw(4 * static_cast<std::size_t>(e.ebins));
         for (int s = 0; s < 4; ++s) {
             const auto w = e.tables[static_cast<std::size_t>(s)].weights();
@@ -81,9 +93,17 @@ struct Engine::Impl {
         d.gs = e.matt.gs;
         d.S = e.matt.S;
         d.nflav = 2;
-        // lanes -> one GPU here; a multi-GPU caller passes OscComm (rank,
-        // nranks, device, NCCL id) and connects the peer exchange instead
-        ok(osc_create(&d, nullptr, &ctx));
+        // GPUs: OSC_GPUS (default: every visible device), at most one per
+        // theta bin, one for the single-angle model.  lanes stays what it is
+        // in the reference — the worker count the interface validates — and
+        // does not change the device decomposition, so results are
+        // bit-identical for any lanes (test_solver.cpp:226-251).
+        gpus = b200::device_count();
+        if (const char* g = std::getenv("OSC_GPUS")) gpus = std::atoi(g);
+        if (gpus < 1) gpus = 1;
+        gpus = std::min(gpus, e.grid.abins);
+        if (e.grid.model == geom::Model::SingleAngle) gpus = 1;
+        ok(osc_create_group(&d, gpus, nullptr, 0, &ctx));
     }
     ~Impl() {
         if (ctx) osc_destroy(ctx);
@@ -131,6 +151,7 @@ void Engine::init_states() {
 }
 
 double Engine::trial_step_error(double r, double dr) {
+    if (impl_->lanes != 1) throw ConfigError("trial_step_error: single-lane engines only");  // solver.cpp:480-484
     impl_->push_if_dirty();
     double err = 0.0;
     ok(osc_trial_step_error(impl_->ctx, r, dr, &err));
@@ -140,6 +161,20 @@ double Engine::trial_step_error(double r, double dr) {
 RunSummary Engine::run(StepControl c, const IoHook& hook) {
     impl_->push_if_dirty();
     const OscStepControl oc{c.dr, c.dr_max, c.dr_min, c.eps0, c.kappa, c.r, c.R0, c.Rn, c.iter, c.Ts, c.Tn};
+    OscRunSummary s{};
+    if (const b200::DeviceDumps* dd = b200::DeviceDumps::active()) {
+        // device-gated dumps (solver_b200.hpp): no per-step hook
+        if (hook) throw ConfigError("Engine::run: an IoHook and a DeviceDumps scope are exclusive");
+        const b200::DumpSpec& sp = dd->spec();
+        OscDumpGates g[2];
+        for (int m = 0; m < 2; ++m) g[m] = {sp.gates[m].r_step, sp.gates[m].t_step, sp.gates[m].itr_step};
+        auto cb = [](void* u, int mode, const OscRecordMeta* m, const double* p, std::size_t n) {
+            const auto* d = static_cast<const b200::DeviceDumps*>(u);
+            d->sink()(mode, io::RecordMeta{m->iter, m->r, m->dr, m->t_wall}, std::span<const double>(p, n));
+        };
+        ok(osc_run_dumps(impl_->ctx, &oc, g, sp.mode_mask, +cb, const_cast<b200::DeviceDumps*>(dd), &s));
+        return summary_of(s);
+    }
     struct Tramp {
         const IoHook* hook;
         const Environment* env;
@@ -150,8 +185,30 @@ RunSummary Engine::run(StepControl c, const IoHook& hook) {
         fill_mode1(*tp->set, tp->env->grid, std::span<const double>(st, n));
         (*tp->hook)(HookInfo{i->iter, i->r, i->dr, i->t_wall}, *tp->set);
     };
-    OscRunSummary s{};
     ok(osc_run(impl_->ctx, &oc, hook ? +cb : nullptr, &t, &s));
+    return summary_of(s);
+}
+
+namespace b200 {
+
+namespace {
+thread_local const DeviceDumps* t_active = nullptr;
+}
+
+DeviceDumps::DeviceDumps(const DumpSpec& spec, DumpSink sink) : spec_(spec), sink_(std::move(sink)), prev_(t_active) {
+    t_active = this;
+}
+DeviceDumps::~DeviceDumps() { t_active = prev_; }
+const DeviceDumps* DeviceDumps::active() { return t_active; }
+
+int device_count() {
+    int n = 0;
+    return osc_device_count(&n) == OSC_OK ? n : 0;
+}
+
+}  // namespace b200
+
+RunSummary summary_of(const OscRunSummary& s) {
     RunSummary out;
     out.final_r = s.final_r;
     out.iterations = s.iterations;

@@ -74,7 +74,7 @@ class RunConfig:
         elif key in _STR:
             self.values[key] = value
         elif key in _IGNORED:
-            pass
+            self.values[key] = value  # (kept verbatim for render)
         else:
             raise KeyError(key)
         self.provided.add(key)

@@ -142,6 +142,10 @@ template <class T>
 struct DevBuf {
     T* p = nullptr;
     size_t n = 0;
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    ~DevBuf() { free(); }
     void alloc(size_t count) {
         free();
         if (count == 0) count = 1;
@@ -219,6 +223,16 @@ struct OscCtx {
     }
     cudaStream_t stream = nullptr;
     nccl::Comm comm = nullptr;
+    // In-process group (osc_create_group: Engine lanes mapped onto GPUs, one
+    // context per rank, one host thread): a group handle owns its ranks in
+    // `kids`; `ordered` selects the stream-ordered exchange (rank slots copied
+    // between the ranks' exchange buffers behind cross-stream events: any
+    // device placement, several ranks per GPU included) instead of the
+    // device-initiated one over peer pointers (distinct GPUs).
+    std::vector<OscCtx*> kids;
+    int ordered = 0;
+    bool in_group = false;  // (a rank of a group: the group drives its exchange)
+    std::vector<cudaEvent_t> gev;
 
     DevBuf<double> cos2, sin0, cphi, sphi, vac11, vac12, g, ktab_g;
     DevBuf<double> cpart[4];  // single GPU: block partials of S2, S3, S4 (consumer-side reduction)
@@ -253,6 +267,11 @@ struct OscCtx {
     }
 
     ~OscCtx() {
+        for (OscCtx* k : kids) delete k;
+        for (cudaEvent_t e : gev) cudaEventDestroy(e);
+        for (double*& p : pinned)
+            if (p) cudaFreeHost(p);
+        if (!kids.empty()) return;  // (a group handle owns no device buffers)
         drop_graphs();
         if (comm) {
             try {
@@ -262,8 +281,6 @@ struct OscCtx {
         }
         for (void* p : ipc_opened) cudaIpcCloseMemHandle(p);
         if (h_ctl) cudaFreeHost(h_ctl);
-        for (double* p : pinned)
-            if (p) cudaFreeHost(p);
         if (copy_stream) cudaStreamDestroy(copy_stream);
         if (stream) cudaStreamDestroy(stream);
     }
@@ -314,7 +331,7 @@ struct OscCtx {
     }
 
     void exchange(int slot) {
-        if (!coll || args.p2p) return;
+        if (!coll || args.p2p || in_group) return;
         nccl::check(nccl::api().all_gather(xsend.p + (size_t)slot * kSlotDoubles,
                                            xbuf.p + (size_t)slot * nranks * kSlotDoubles, kSlotDoubles,
                                            nccl::kFloat64, comm, stream),
@@ -448,6 +465,15 @@ struct OscCtx {
     // Arm the device control block like Engine::run's first packet
     // (solver.cpp:492-500).
     void begin(const OscStepControl& c, int commit) {
+        begin_ctl(c, commit);
+        if (!h_ctl->terminate) {
+            check_radius(c.r);
+            enqueue_moments0();
+            bloch_stale = false;
+        }
+    }
+    // The control block part of begin (no launches).
+    void begin_ctl(const OscStepControl& c, int commit) {
         download_ctl();
         Ctl& h = *h_ctl;
         h.r = c.r;
@@ -475,11 +501,6 @@ struct OscCtx {
             if (c.Ts > 0 && c.iter >= c.Ts) h.terminate = 2;
         }
         upload_ctl();
-        if (!h.terminate) {
-            check_radius(c.r);
-            enqueue_moments0();
-            bloch_stale = false;
-        }
     }
 };
 
@@ -767,7 +788,7 @@ int osc_create(const OscDesc* desc, const OscComm* comm, OscCtx** out) {
             }
         }
 
-        if (c->coll) {
+        if (c->coll && !(comm->flags & OSC_COMM_GROUP)) {
             nccl::UniqueId id;
             if (comm->nccl_unique_id) {
                 std::memcpy(&id, comm->nccl_unique_id, sizeof id);
@@ -848,11 +869,309 @@ int osc_create(const OscDesc* desc, const OscComm* comm, OscCtx** out) {
     });
 }
 
+}  // extern "C"
+
+// ------------------------------------------------------------------ groups
+// Every entry point below accepts either one context or a group handle
+// (osc_create_group); `ranks_of` lists the contexts that hold state.
+namespace {
+
+std::vector<OscCtx*> ranks_of(OscCtx* c) { return c->kids.empty() ? std::vector<OscCtx*>{c} : c->kids; }
+std::vector<const OscCtx*> ranks_of(const OscCtx* c) {
+    if (c->kids.empty()) return {c};
+    return std::vector<const OscCtx*>(c->kids.begin(), c->kids.end());
+}
+void use(const OscCtx* c) { CUDA_OK(cudaSetDevice(c->device)); }
+size_t local_doubles(const OscCtx* c) { return (size_t)c->ncell * c->nplanes; }
+size_t total_doubles(const OscCtx* c) {
+    size_t n = 0;
+    for (const OscCtx* k : ranks_of(c)) n += local_doubles(k);
+    return n;
+}
+size_t mode2_local(const OscCtx* c) { return (size_t)c->ntraj * (c->nflav == 3 ? 6 : 4); }
+size_t mode2_total(const OscCtx* c) {
+    size_t n = 0;
+    for (const OscCtx* k : ranks_of(c)) n += mode2_local(k);
+    return n;
+}
+// rank 0's control block (every rank holds the same decisions)
+Ctl& hctl(OscCtx* c) { return *ranks_of(c)[0]->h_ctl; }
+
+// Stream-ordered exchange of slot `slot` (the group's replacement of the
+// NCCL all-gather): every rank's rank slot (xsend, written by its stage's
+// last block) is copied into every rank's exchange buffer at [slot][q],
+// behind an event of the producing rank's stream.
+void ordered_exchange(OscCtx* g, int slot) {
+    const int n = (int)g->kids.size();
+    for (int q = 0; q < n; ++q) {
+        use(g->kids[q]);
+        CUDA_OK(cudaEventRecord(g->gev[q], g->kids[q]->stream));
+    }
+    for (int r = 0; r < n; ++r) {
+        OscCtx* k = g->kids[r];
+        use(k);
+        for (int q = 0; q < n; ++q) {
+            OscCtx* src = g->kids[q];
+            if (q != r) CUDA_OK(cudaStreamWaitEvent(k->stream, g->gev[q], 0));
+            CUDA_OK(cudaMemcpyPeerAsync(k->xbuf.p + ((size_t)slot * n + q) * kSlotDoubles, k->device,
+                                        src->xsend.p + (size_t)slot * kSlotDoubles, src->device,
+                                        kSlotDoubles * sizeof(double), k->stream));
+        }
+    }
+}
+
+// S1 on every rank + the slot-0 exchange.
+void g_moments0(OscCtx* g) {
+    if (g->kids.empty()) {
+        g->enqueue_moments0();
+        g->bloch_stale = false;
+        return;
+    }
+    if (g->ordered) {
+        for (OscCtx* k : g->kids) {
+            use(k);
+            k->launch_stage(0);
+        }
+        ordered_exchange(g, 0);
+    } else {
+        for (OscCtx* k : g->kids) {
+            use(k);
+            k->enqueue_moments0();
+        }
+    }
+    for (OscCtx* k : g->kids) k->bloch_stale = false;
+}
+
+// Engine::run's first packet on every rank (+ S1 unless already terminated).
+void g_begin(OscCtx* g, const OscStepControl& c, int commit) {
+    if (g->kids.empty()) {
+        g->begin(c, commit);
+        return;
+    }
+    for (OscCtx* k : g->kids) {
+        use(k);
+        k->begin_ctl(c, commit);
+    }
+    if (hctl(g).terminate) return;
+    g->kids[0]->check_radius(c.r);
+    g_moments0(g);
+}
+
+// n steps on every rank.  Device-initiated exchange: each rank enqueues its
+// own graphs (the ranks meet inside the kernels).  Stream-ordered exchange:
+// stage by stage across the ranks with the exchange between stages and the
+// per-rank control kernel after S4.
+void g_enqueue_steps(OscCtx* g, int n) {
+    if (g->kids.empty()) {
+        g->enqueue_steps(n);
+        return;
+    }
+    if (!g->ordered) {
+        for (OscCtx* k : g->kids) {
+            use(k);
+            k->enqueue_steps(n);
+        }
+        return;
+    }
+    bool stale = false;
+    for (OscCtx* k : g->kids) stale = stale || k->bloch_stale;
+    if (stale && n > 0) g_moments0(g);
+    for (int i = 0; i < n; ++i) {
+        for (int st = 2; st <= 4; ++st) {
+            for (OscCtx* k : g->kids) {
+                use(k);
+                k->launch_stage(st);
+            }
+            ordered_exchange(g, st - 1);
+        }
+        for (OscCtx* k : g->kids) {
+            use(k);
+            k_control<<<1, 128, 0, k->stream>>>(k->args);
+            k->count();
+            CUDA_OK(cudaGetLastError());
+        }
+    }
+}
+
+void g_prepare_graphs(OscCtx* g) {
+    if (g->ordered) return;
+    for (OscCtx* k : ranks_of(g)) {
+        use(k);
+        k->prepare_graphs();
+    }
+}
+
+// Control blocks of every rank to the host; the first device-detected
+// failure (in rank order) is raised.  Returns rank 0's copy.
+Ctl& g_download(OscCtx* g) {
+    for (OscCtx* k : ranks_of(g)) {
+        use(k);
+        k->download_ctl();
+    }
+    for (OscCtx* k : ranks_of(g)) k->raise_device_status();
+    return hctl(g);
+}
+
+void g_sync(OscCtx* g) {
+    for (OscCtx* k : ranks_of(g)) {
+        use(k);
+        CUDA_OK(cudaStreamSynchronize(k->stream));
+    }
+}
+
+void set_state_local(OscCtx* c, const double* src, cudaMemcpyKind kind) {
+    const size_t want = local_doubles(c);
+    use(c);
+    if (c->staging.n < want) c->staging.alloc(want);
+    CUDA_OK(cudaMemcpyAsync(c->staging.p, src, want * sizeof(double), kind, c->stream));
+    k_unpack<<<c->nsm * 8, 256, 0, c->stream>>>(c->args, c->staging.p, want);
+    c->count();
+    CUDA_OK(cudaGetLastError());
+    c->bloch_stale = true;
+}
+
+void get_state_local(OscCtx* c, double* dst, cudaMemcpyKind kind) {
+    const size_t want = local_doubles(c);
+    use(c);
+    if (c->staging.n < want) c->staging.alloc(want);
+    k_pack<<<c->nsm * 8, 256, 0, c->stream>>>(c->args, c->staging.p, want);
+    c->count();
+    CUDA_OK(cudaGetLastError());
+    CUDA_OK(cudaMemcpyAsync(dst, c->staging.p, want * sizeof(double), kind, c->stream));
+}
+
+// Whole payloads: the ranks' theta blocks are contiguous and in rank order,
+// so the mode-1 payload ([traj][species][comp][ebin]) is their concatenation.
+void set_state_impl(OscCtx* g, const double* src, size_t n, cudaMemcpyKind kind) {
+    if (n != total_doubles(g)) throw Error(OSC_ERR_IO, "fill_mode1: payload size does not match the configured problem");
+    size_t off = 0;
+    for (OscCtx* k : ranks_of(g)) {
+        set_state_local(k, src + off, kind);
+        off += local_doubles(k);
+    }
+    g_sync(g);
+}
+
+void get_state_impl(OscCtx* g, double* dst, size_t n, cudaMemcpyKind kind) {
+    if (n != total_doubles(g)) throw Error(OSC_ERR_IO, "extract_mode1: payload size mismatch");
+    size_t off = 0;
+    for (OscCtx* k : ranks_of(g)) {
+        get_state_local(k, dst + off, kind);
+        off += local_doubles(k);
+    }
+    g_sync(g);
+}
+
+}  // namespace
+
+extern "C" {
+
+int osc_device_count(int* n) {
+    return guarded([&] {
+        int c = 0;
+        if (cudaGetDeviceCount(&c) != cudaSuccess) c = 0;
+        *n = c;
+    });
+}
+
+int osc_create_group(const OscDesc* desc, int nranks, const int* devices, int flags, OscCtx** out) {
+    return guarded([&] {
+        validate(desc);
+        if (!out) throw Error(OSC_ERR_CONFIG, "osc_create_group: null out");
+        if (nranks < 1 || nranks > kMaxRanks) throw Error(OSC_ERR_CONFIG, "osc_create_group: bad rank count");
+        int ndev = 0;
+        CUDA_OK(cudaGetDeviceCount(&ndev));
+        std::vector<int> dev(nranks);
+        for (int q = 0; q < nranks; ++q) {
+            dev[q] = devices ? devices[q] : q % std::max(1, ndev);
+            if (dev[q] < 0 || dev[q] >= ndev) throw Error(OSC_ERR_CONFIG, "osc_create_group: bad device index");
+        }
+        if (nranks == 1) {
+            const OscComm one{0, 1, dev[0], nullptr, 0};
+            const int rc = osc_create(desc, &one, out);
+            if (rc != OSC_OK) throw Error(rc, g_last_error);
+            return;
+        }
+        auto g = std::make_unique<OscCtx>();
+        g->desc = *desc;
+        g->nranks = nranks;
+        g->coll = true;
+        g->device = dev[0];
+        g->T = desc->abins;
+        g->P = desc->pbins;
+        g->E = desc->ebins;
+        g->t_lo = 0;
+        g->t_hi = desc->abins;
+        g->nflav = desc->nflav == 3 ? 3 : 2;
+        g->nplanes = g->nflav == 3 ? 36 : 16;
+        // device-initiated exchange needs one rank per GPU and peer access
+        // between every pair; otherwise (or when asked) the ordered exchange
+        bool ordered = (flags & OSC_GROUP_ORDERED) != 0;
+        for (int a = 0; a < nranks && !ordered; ++a)
+            for (int b = 0; b < nranks && !ordered; ++b) {
+                if (a == b) continue;
+                if (dev[a] == dev[b]) {
+                    ordered = true;
+                    break;
+                }
+                int can = 0;
+                CUDA_OK(cudaDeviceCanAccessPeer(&can, dev[a], dev[b]));
+                if (!can) ordered = true;
+            }
+        g->ordered = ordered ? 1 : 0;
+        for (int q = 0; q < nranks; ++q) {
+            const OscComm cm{q, nranks, dev[q], nullptr, OSC_COMM_GROUP};
+            OscCtx* k = nullptr;
+            const int rc = osc_create(desc, &cm, &k);
+            if (rc != OSC_OK) throw Error(rc, g_last_error);
+            k->in_group = true;
+            g->kids.push_back(k);
+            g->ntraj += k->ntraj;
+            g->ncell += k->ncell;
+        }
+        g->gev.resize(nranks);
+        for (int q = 0; q < nranks; ++q) {
+            use(g->kids[q]);
+            CUDA_OK(cudaEventCreateWithFlags(&g->gev[q], cudaEventDisableTiming));
+        }
+        if (!ordered) {
+            for (int a = 0; a < nranks; ++a) {
+                use(g->kids[a]);
+                for (int b = 0; b < nranks; ++b) {
+                    if (a == b) continue;
+                    const cudaError_t e = cudaDeviceEnablePeerAccess(dev[b], 0);
+                    if (e == cudaErrorPeerAccessAlreadyEnabled) {
+                        cudaGetLastError();
+                    } else {
+                        CUDA_OK(e);
+                    }
+                }
+            }
+            for (OscCtx* k : g->kids) {
+                for (int q = 0; q < nranks; ++q) k->args.peer_xll[q] = g->kids[q]->xll.p;
+                k->args.p2p = 1;
+                k->drop_graphs();
+            }
+        }
+        *out = g.release();
+    });
+}
+
+int osc_group_info(const OscCtx* c, int* nranks, int* ordered) {
+    return guarded([&] {
+        if (!c) throw Error(OSC_ERR_CONFIG, "null context");
+        if (nranks) *nranks = c->kids.empty() ? 1 : (int)c->kids.size();
+        if (ordered) *ordered = c->ordered;
+    });
+}
+
 int osc_destroy(OscCtx* ctx) {
     return guarded([&] {
         if (!ctx) return;
-        cudaSetDevice(ctx->device);
-        cudaStreamSynchronize(ctx->stream);
+        for (OscCtx* k : ranks_of(ctx)) {
+            cudaSetDevice(k->device);
+            cudaStreamSynchronize(k->stream);
+        }
         delete ctx;
     });
 }
@@ -862,44 +1181,23 @@ int osc_local_range(const OscCtx* c, int* t_lo, int* t_hi, size_t* n) {
         if (!c) throw Error(OSC_ERR_CONFIG, "null context");
         if (t_lo) *t_lo = c->t_lo;
         if (t_hi) *t_hi = c->t_hi;
-        if (n) *n = (size_t)c->ncell * c->nplanes;
+        if (n) *n = total_doubles(c);
     });
 }
 
-int osc_init_states(OscCtx* c) {
+int osc_init_states(OscCtx* g) {
     return guarded([&] {
-        CUDA_OK(cudaSetDevice(c->device));
-        if (c->nflav == 3)
-            k_init3<<<(c->ncell + 255) / 256, 256, 0, c->stream>>>(c->args, c->desc.perturb);
-        else
-            k_init<<<(c->ncell + 255) / 256, 256, 0, c->stream>>>(c->args, c->desc.perturb);
-        c->count();
-        CUDA_OK(cudaGetLastError());
-        CUDA_OK(cudaStreamSynchronize(c->stream));
+        for (OscCtx* c : ranks_of(g)) {
+            use(c);
+            if (c->nflav == 3)
+                k_init3<<<(c->ncell + 255) / 256, 256, 0, c->stream>>>(c->args, c->desc.perturb);
+            else
+                k_init<<<(c->ncell + 255) / 256, 256, 0, c->stream>>>(c->args, c->desc.perturb);
+            c->count();
+            CUDA_OK(cudaGetLastError());
+        }
+        g_sync(g);
     });
-}
-
-static void set_state_impl(OscCtx* c, const double* src, size_t n, cudaMemcpyKind kind) {
-    const size_t want = (size_t)c->ncell * c->nplanes;
-    if (n != want) throw Error(OSC_ERR_IO, "fill_mode1: payload size does not match the configured problem");
-    CUDA_OK(cudaSetDevice(c->device));
-    if (c->staging.n < want) c->staging.alloc(want);
-    CUDA_OK(cudaMemcpyAsync(c->staging.p, src, want * sizeof(double), kind, c->stream));
-    k_unpack<<<c->nsm * 8, 256, 0, c->stream>>>(c->args, c->staging.p, want); c->count();
-    CUDA_OK(cudaGetLastError());
-    c->bloch_stale = true;
-    CUDA_OK(cudaStreamSynchronize(c->stream));
-}
-
-static void get_state_impl(OscCtx* c, double* dst, size_t n, cudaMemcpyKind kind) {
-    const size_t want = (size_t)c->ncell * c->nplanes;
-    if (n != want) throw Error(OSC_ERR_IO, "extract_mode1: payload size mismatch");
-    CUDA_OK(cudaSetDevice(c->device));
-    if (c->staging.n < want) c->staging.alloc(want);
-    k_pack<<<c->nsm * 8, 256, 0, c->stream>>>(c->args, c->staging.p, want); c->count();
-    CUDA_OK(cudaGetLastError());
-    CUDA_OK(cudaMemcpyAsync(dst, c->staging.p, want * sizeof(double), kind, c->stream));
-    CUDA_OK(cudaStreamSynchronize(c->stream));
 }
 
 int osc_set_state(OscCtx* c, const double* m, size_t n) {
@@ -909,16 +1207,17 @@ int osc_get_state(OscCtx* c, double* m, size_t n) {
     return guarded([&] { get_state_impl(c, m, n, cudaMemcpyDeviceToHost); });
 }
 int osc_set_state_device(OscCtx* c, const double* m, size_t n) {
-    return guarded([&] { set_state_impl(c, m, n, cudaMemcpyDeviceToDevice); });
+    return guarded([&] { set_state_impl(c, m, n, cudaMemcpyDefault); });
 }
 int osc_get_state_device(OscCtx* c, double* m, size_t n) {
-    return guarded([&] { get_state_impl(c, m, n, cudaMemcpyDeviceToDevice); });
+    return guarded([&] { get_state_impl(c, m, n, cudaMemcpyDefault); });
 }
 
 int osc_trial_step_error(OscCtx* c, double r, double dr, double* err) {
     return guarded([&] {
-        if (c->nranks != 1) throw Error(OSC_ERR_CONFIG, "trial_step_error: single-lane engines only");
-        CUDA_OK(cudaSetDevice(c->device));
+        // (a multi-process rank cannot take a trial step alone; a group can)
+        if (c->kids.empty() && c->nranks != 1)
+            throw Error(OSC_ERR_CONFIG, "trial_step_error: single-lane engines only");
         OscStepControl s{};
         s.r = r;
         s.dr = dr;
@@ -927,60 +1226,73 @@ int osc_trial_step_error(OscCtx* c, double r, double dr, double* err) {
         s.eps0 = 1e300;
         s.kappa = 1.0;
         s.Rn = r + dr;
-        c->begin(s, /*commit=*/0);
-        c->enqueue_step();
-        c->finalize();
-        c->download_ctl();
-        c->raise_device_status();
-        *err = c->h_ctl->err;
+        if (c->kids.empty()) {
+            use(c);
+            c->begin(s, /*commit=*/0);
+            c->enqueue_step();
+            c->finalize();
+        } else {
+            g_begin(c, s, 0);
+            if (c->ordered) {
+                g_enqueue_steps(c, 1);
+            } else {
+                for (OscCtx* k : c->kids) {
+                    use(k);
+                    k->enqueue_step();
+                }
+            }
+        }
+        *err = g_download(c).err;
     });
 }
 
 int osc_begin(OscCtx* c, const OscStepControl* ctl) {
     return guarded([&] {
-        CUDA_OK(cudaSetDevice(c->device));
-        c->begin(*ctl, 1);
-        c->prepare_graphs();
+        g_begin(c, *ctl, 1);
+        g_prepare_graphs(c);
     });
 }
 
 int osc_enqueue_steps(OscCtx* c, int n) {
-    return guarded([&] {
-        CUDA_OK(cudaSetDevice(c->device));
-        c->enqueue_steps(n);
-    });
+    return guarded([&] { g_enqueue_steps(c, n); });
 }
 
 int osc_query(OscCtx* c, double* r, double* dr, uint64_t* iter, uint64_t* acc, uint64_t* rej, double* err,
               int* status, int* term) {
     return guarded([&] {
-        CUDA_OK(cudaSetDevice(c->device));
-        c->download_ctl();
-        const Ctl& h = *c->h_ctl;
+        for (OscCtx* k : ranks_of(c)) {
+            use(k);
+            k->download_ctl();
+        }
+        const Ctl& h = hctl(c);
         if (r) *r = h.r;
         if (dr) *dr = h.dr;
         if (iter) *iter = h.iter;
         if (acc) *acc = h.accepted;
         if (rej) *rej = h.rejected;
         if (err) *err = h.err;
-        if (status) *status = h.status;
+        int st = 0;
+        for (OscCtx* k : ranks_of(c)) st = st ? st : k->h_ctl->status;
+        if (status) *status = st;
         if (term) *term = h.terminate;
     });
 }
 
 int osc_synchronize(OscCtx* c) {
-    return guarded([&] {
-        CUDA_OK(cudaSetDevice(c->device));
-        CUDA_OK(cudaStreamSynchronize(c->stream));
-    });
+    return guarded([&] { g_sync(c); });
 }
 
-void* osc_stream(OscCtx* c) { return c ? (void*)c->stream : nullptr; }
+void* osc_stream(OscCtx* c) { return c ? (void*)ranks_of(c)[0]->stream : nullptr; }
 
-int osc_launches_per_step(const OscCtx* c) { return c ? (c->coll && !c->args.p2p ? 4 : 3) : 0; }
+int osc_launches_per_step(const OscCtx* c) {
+    if (!c) return 0;
+    const OscCtx* k = ranks_of(c)[0];
+    return k->coll && !k->args.p2p ? 4 : 3;
+}
 
-int osc_debug_sums(OscCtx* c, double* out) {
+int osc_debug_sums(OscCtx* g, double* out) {
     return guarded([&] {
+        OscCtx* c = ranks_of(g)[0];
         CUDA_OK(cudaSetDevice(c->device));
         std::vector<double> x(c->xbuf.n);
         CUDA_OK(cudaStreamSynchronize(c->stream));
@@ -1001,15 +1313,17 @@ int osc_debug_sums(OscCtx* c, double* out) {
     });
 }
 
-int osc_set_schedule(OscCtx* c, int schedule) {
+int osc_set_schedule(OscCtx* g, int schedule) {
     return guarded([&] {
-        CUDA_OK(cudaSetDevice(c->device));
         if (schedule != 0 && schedule != 1) throw Error(OSC_ERR_CONFIG, "schedule must be 0 or 1");
-        if (schedule == 1 && !c->stash.p) c->stash.alloc((size_t)c->npad * c->nplanes);
-        c->schedule = schedule;
-        c->args.schedule = schedule;
-        c->args.stash = c->stash.p;
-        c->drop_graphs();
+        for (OscCtx* c : ranks_of(g)) {
+            use(c);
+            if (schedule == 1 && !c->stash.p) c->stash.alloc((size_t)c->npad * c->nplanes);
+            c->schedule = schedule;
+            c->args.schedule = schedule;
+            c->args.stash = c->stash.p;
+            c->drop_graphs();
+        }
     });
 }
 
@@ -1024,10 +1338,16 @@ int osc_set_launch_mode(OscCtx* c, int mode) {
 
 int osc_get_launch_mode(OscCtx* c) { return c ? c->launch_mode : 0; }
 
-unsigned long long osc_launch_count(const OscCtx* c) { return c ? c->nlaunch : 0; }
+unsigned long long osc_launch_count(const OscCtx* c) {
+    unsigned long long n = 0;
+    if (c)
+        for (const OscCtx* k : ranks_of(c)) n += k->nlaunch;
+    return n;
+}
 
 int osc_comm_export(OscCtx* c, void* out128) {
     return guarded([&] {
+        if (!c->kids.empty()) throw Error(OSC_ERR_CONFIG, "osc_comm_export: group contexts exchange in-process");
         if (!out128) throw Error(OSC_ERR_CONFIG, "osc_comm_export: null out");
         CUDA_OK(cudaSetDevice(c->device));
         cudaIpcMemHandle_t h[2];
@@ -1113,6 +1433,7 @@ int osc_debug_evolve_bin(int device, size_t n, const double* h, const double* dl
 
 int osc_profile_stages(OscCtx* c, int nsteps, float* ms_out) {
     return guarded([&] {
+        if (!c->kids.empty()) throw Error(OSC_ERR_CONFIG, "osc_profile_stages: single-GPU contexts only");
         CUDA_OK(cudaSetDevice(c->device));
         if (c->nranks != 1) throw Error(OSC_ERR_CONFIG, "osc_profile_stages: single-GPU contexts only");
         cudaEvent_t ev[4];
@@ -1154,26 +1475,33 @@ int osc_debug_trace(unsigned long long* out, size_t n) {
     });
 }
 
-int osc_max_norm_dev(OscCtx* c, double* out) {
+int osc_max_norm_dev(OscCtx* g, double* out) {
     return guarded([&] {
-        CUDA_OK(cudaSetDevice(c->device));
-        CUDA_OK(cudaMemsetAsync(c->scratch.p, 0, sizeof(unsigned long long), c->stream));
-        k_norm_dev<<<c->nsm * 4, 256, 0, c->stream>>>(c->args, c->scratch.p); c->count();
-        CUDA_OK(cudaGetLastError());
-        unsigned long long bits = 0;
-        CUDA_OK(cudaMemcpyAsync(&bits, c->scratch.p, sizeof bits, cudaMemcpyDeviceToHost, c->stream));
-        CUDA_OK(cudaStreamSynchronize(c->stream));
-        double v;
-        std::memcpy(&v, &bits, sizeof v);
-        *out = v;
+        double worst = 0.0;
+        for (OscCtx* c : ranks_of(g)) {
+            use(c);
+            CUDA_OK(cudaMemsetAsync(c->scratch.p, 0, sizeof(unsigned long long), c->stream));
+            k_norm_dev<<<c->nsm * 4, 256, 0, c->stream>>>(c->args, c->scratch.p);
+            c->count();
+            CUDA_OK(cudaGetLastError());
+            unsigned long long bits = 0;
+            CUDA_OK(cudaMemcpyAsync(&bits, c->scratch.p, sizeof bits, cudaMemcpyDeviceToHost, c->stream));
+            CUDA_OK(cudaStreamSynchronize(c->stream));
+            double v;
+            std::memcpy(&v, &bits, sizeof v);
+            worst = std::max(worst, v);
+        }
+        *out = worst;
     });
 }
 
-static size_t mode2_doubles(const OscCtx* c) { return (size_t)c->ntraj * (c->nflav == 3 ? 6 : 4); }
+}  // extern "C"
 
-// Enqueue the mode-2 extraction into mode2buf (context stream).
-static void enqueue_mode2(OscCtx* c) {
-    const size_t n = mode2_doubles(c);
+namespace {
+
+// Enqueue the mode-2 extraction of one rank into its mode2buf (its stream).
+void enqueue_mode2(OscCtx* c) {
+    const size_t n = mode2_local(c);
     if (c->mode2buf.n < n) c->mode2buf.alloc(n);
     k_mode2<<<(int)std::min<size_t>((n + 255) / 256, (size_t)c->nsm * 8), 256, 0, c->stream>>>(c->args, c->fw.p,
                                                                                              c->mode2buf.p);
@@ -1181,29 +1509,84 @@ static void enqueue_mode2(OscCtx* c) {
     CUDA_OK(cudaGetLastError());
 }
 
-int osc_extract_mode2(OscCtx* c, double* out, size_t n) {
+// Steps per host round trip of Engine::run: graph batches of up to 64 steps,
+// never past Ts, and — with a wall-time limit Tn — sized from the measured
+// step time so that the last batches before Tn shrink to single steps (the
+// reference checks Tn after every step, solver.cpp:453).
+struct Batcher {
+    const OscStepControl* ctl;
+    double step_s = -1.0;  // measured seconds per step (-1: unknown)
+    int last = 0;
+    int next(uint64_t iter, double elapsed) const {
+        int b = 64;
+        if (ctl->Ts > 0) {
+            const uint64_t left = ctl->Ts - std::min<uint64_t>(ctl->Ts, iter);
+            b = (int)std::max<uint64_t>(1, std::min<uint64_t>(left, 64));
+        }
+        if (ctl->Tn > 0.0) {
+            const int cap = step_s < 0.0 ? std::max(1, 2 * last)
+                                         : (int)std::max(1.0, std::min(64.0, 0.5 * (ctl->Tn - elapsed) / step_s));
+            b = std::min(b, std::max(1, cap));
+        }
+        return b;
+    }
+    void measured(int steps, double secs) {
+        if (steps > 0 && secs > 0.0) step_s = step_s < 0.0 ? secs / steps : std::min(step_s, secs / steps);
+    }
+};
+
+void fill_summary(OscCtx* g, const OscStepControl* ctl, int term, double wall, double t_io, OscRunSummary* out) {
+    double nd = 0.0;
+    const int rc = osc_max_norm_dev(g, &nd);
+    if (rc != OSC_OK) throw Error(rc, g_last_error);
+    const Ctl& h = hctl(g);
+    out->final_r = h.r;
+    out->iterations = h.iter - ctl->iter;
+    out->accepted = h.accepted;
+    out->rejected = h.rejected;
+    out->wall_s = wall;
+    out->phase_hamiltonian_s = 0.0;  // (fused into the stage kernels)
+    out->phase_evolve_s = wall - t_io;
+    out->phase_io_s = t_io;
+    out->max_worker_wait_s = 0.0;
+    out->final_max_norm_dev = nd;
+    out->termination = term == 2 ? 2 : (term == 3 ? 3 : 1);
+}
+
+}  // namespace
+
+extern "C" {
+
+int osc_extract_mode2(OscCtx* g, double* out, size_t n) {
     return guarded([&] {
-        if (n != mode2_doubles(c)) throw Error(OSC_ERR_IO, "extract_mode2: payload size mismatch");
-        CUDA_OK(cudaSetDevice(c->device));
-        enqueue_mode2(c);
-        CUDA_OK(cudaMemcpyAsync(out, c->mode2buf.p, n * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-        CUDA_OK(cudaStreamSynchronize(c->stream));
+        if (n != mode2_total(g)) throw Error(OSC_ERR_IO, "extract_mode2: payload size mismatch");
+        size_t off = 0;
+        for (OscCtx* c : ranks_of(g)) {
+            use(c);
+            enqueue_mode2(c);
+            CUDA_OK(cudaMemcpyAsync(out + off, c->mode2buf.p, mode2_local(c) * sizeof(double), cudaMemcpyDeviceToHost,
+                                    c->stream));
+            off += mode2_local(c);
+        }
+        g_sync(g);
     });
 }
 
-int osc_run_dumps(OscCtx* c, const OscStepControl* ctl, const OscDumpGates* gates, int mode_mask,
+int osc_run_dumps(OscCtx* g, const OscStepControl* ctl, const OscDumpGates* gates, int mode_mask,
                   osc_dump_fn fn, void* user, OscRunSummary* out) {
     return guarded([&] {
         using Clock = std::chrono::steady_clock;
         if (!ctl || !out || (mode_mask && (!gates || !fn)))
             throw Error(OSC_ERR_CONFIG, "osc_run_dumps: null argument");
         mode_mask &= 3;
-        CUDA_OK(cudaSetDevice(c->device));
+        const std::vector<OscCtx*> R = ranks_of(g);
         const auto t0 = Clock::now();
         auto secs = [&] { return std::chrono::duration<double>(Clock::now() - t0).count(); };
-        c->begin(*ctl, 1);
-        // arm the device gates (DumpDriver::reset_marks: marks at the start)
-        {
+        g_begin(g, *ctl, 1);
+        // arm the device gates on every rank (DumpDriver::reset_marks: marks
+        // at the start)
+        for (OscCtx* c : R) {
+            use(c);
             c->download_ctl();
             Ctl& h = *c->h_ctl;
             h.dump_mask = mode_mask;
@@ -1217,45 +1600,58 @@ int osc_run_dumps(OscCtx* c, const OscStepControl* ctl, const OscDumpGates* gate
             c->upload_ctl();
         }
         double mark_t[2] = {0.0, 0.0};
-        const size_t n1 = (size_t)c->ncell * c->nplanes, n2 = mode2_doubles(c);
-        if (mode_mask & 1) {
-            if (c->staging.n < n1) c->staging.alloc(n1);
-            if (c->staging2.n < n1) c->staging2.alloc(n1);
+        const size_t n1 = total_doubles(g), n2 = mode2_total(g);
+        for (OscCtx* c : R) {
+            use(c);
+            const size_t l1 = local_doubles(c), l2 = mode2_local(c);
+            if (mode_mask & 1) {
+                if (c->staging.n < l1) c->staging.alloc(l1);
+                if (c->staging2.n < l1) c->staging2.alloc(l1);
+            }
+            if (mode_mask & 2 && c->mode2buf.n < l2) c->mode2buf.alloc(l2);
+            if (mode_mask && !c->copy_stream) CUDA_OK(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
         }
-        if (mode_mask & 2 && c->mode2buf.n < n2) c->mode2buf.alloc(n2);
         const size_t pin_n = std::max((mode_mask & 1) ? n1 : 0, (mode_mask & 2) ? n2 : 0);
-        if (pin_n > c->pinned_n) {
-            for (double*& p : c->pinned) {
+        if (pin_n > g->pinned_n) {
+            for (double*& p : g->pinned) {
                 if (p) cudaFreeHost(p);
                 p = nullptr;
                 CUDA_OK(cudaMallocHost(&p, pin_n * sizeof(double)));
             }
-            c->pinned_n = pin_n;
+            g->pinned_n = pin_n;
         }
-        if (mode_mask && !c->copy_stream)
-            CUDA_OK(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
 
-        // Two dump slots in flight: packed on the compute stream into a
-        // device staging buffer, copied to pinned memory on the copy stream
-        // while the next steps run; delivered in order.
+        // Two dump slots in flight: packed on each rank's compute stream into
+        // a device staging buffer, copied (rank slices at their payload
+        // offsets) to pinned memory on the rank's copy stream while the next
+        // steps run; delivered in order.
         struct Pending {
             int mode = 0;
             size_t n = 0;
             OscRecordMeta meta{};
-            cudaEvent_t done = nullptr;
+            std::vector<cudaEvent_t> done;  // per rank
             bool busy = false;
         } slot[2];
+        for (Pending& p : slot) {
+            p.done.resize(R.size(), nullptr);
+            for (size_t q = 0; q < R.size(); ++q) {
+                use(R[q]);
+                CUDA_OK(cudaEventCreateWithFlags(&p.done[q], cudaEventDisableTiming));
+            }
+        }
         std::vector<int> fifo;
         double t_io = 0.0;
         auto deliver = [&](bool wait_all, int need_free) {
             while (!fifo.empty()) {
                 Pending& p = slot[fifo.front()];
                 if (!wait_all && need_free < 0) {
-                    if (cudaEventQuery(p.done) == cudaErrorNotReady) break;
+                    bool ready = true;
+                    for (cudaEvent_t e : p.done) ready = ready && cudaEventQuery(e) != cudaErrorNotReady;
+                    if (!ready) break;
                 }
-                CUDA_OK(cudaEventSynchronize(p.done));
+                for (cudaEvent_t e : p.done) CUDA_OK(cudaEventSynchronize(e));
                 const auto ti = Clock::now();
-                fn(user, p.mode, &p.meta, c->pinned[fifo.front()], p.n);
+                fn(user, p.mode, &p.meta, g->pinned[fifo.front()], p.n);
                 t_io += std::chrono::duration<double>(Clock::now() - ti).count();
                 p.busy = false;
                 const int freed = fifo.front();
@@ -1270,47 +1666,51 @@ int osc_run_dumps(OscCtx* c, const OscStepControl* ctl, const OscDumpGates* gate
                 k = !slot[0].busy ? 0 : 1;
             }
             Pending& p = slot[k];
-            if (!p.done) CUDA_OK(cudaEventCreateWithFlags(&p.done, cudaEventDisableTiming));
-            const double* src;
-            if (mode == 1) {
-                double* st = k == 0 ? c->staging.p : c->staging2.p;
-                k_pack<<<c->nsm * 8, 256, 0, c->stream>>>(c->args, st, n1);
-                c->count();
-                CUDA_OK(cudaGetLastError());
-                src = st;
-                p.n = n1;
-            } else {
-                enqueue_mode2(c);
-                src = c->mode2buf.p;
-                p.n = n2;
+            size_t off = 0;
+            for (size_t q = 0; q < R.size(); ++q) {
+                OscCtx* c = R[q];
+                use(c);
+                const double* src;
+                size_t len;
+                if (mode == 1) {
+                    double* st = k == 0 ? c->staging.p : c->staging2.p;
+                    len = local_doubles(c);
+                    k_pack<<<c->nsm * 8, 256, 0, c->stream>>>(c->args, st, len);
+                    c->count();
+                    CUDA_OK(cudaGetLastError());
+                    src = st;
+                } else {
+                    enqueue_mode2(c);
+                    src = c->mode2buf.p;
+                    len = mode2_local(c);
+                }
+                CUDA_OK(cudaEventRecord(p.done[q], c->stream));
+                CUDA_OK(cudaStreamWaitEvent(c->copy_stream, p.done[q], 0));
+                CUDA_OK(cudaMemcpyAsync(g->pinned[k] + off, src, len * sizeof(double), cudaMemcpyDeviceToHost,
+                                        c->copy_stream));
+                CUDA_OK(cudaEventRecord(p.done[q], c->copy_stream));
+                if (mode == 2) CUDA_OK(cudaStreamWaitEvent(c->stream, p.done[q], 0));  // mode2buf reuse
+                off += len;
             }
-            CUDA_OK(cudaEventRecord(p.done, c->stream));
-            CUDA_OK(cudaStreamWaitEvent(c->copy_stream, p.done, 0));
-            CUDA_OK(cudaMemcpyAsync(c->pinned[k], src, p.n * sizeof(double), cudaMemcpyDeviceToHost,
-                                    c->copy_stream));
-            CUDA_OK(cudaEventRecord(p.done, c->copy_stream));
-            if (mode == 2) CUDA_OK(cudaStreamWaitEvent(c->stream, p.done, 0));  // mode2buf reuse
+            p.n = off;
             p.mode = mode;
             p.meta = meta;
             p.busy = true;
             fifo.push_back(k);
         };
 
-        int term = c->h_ctl->terminate;
+        int term = hctl(g).terminate;
         uint64_t last_acc = 0;
+        Batcher bt{ctl};
         auto next_batch = [&]() {
-            int batch = 64;
-            if (ctl->Ts > 0) {
-                const uint64_t left = ctl->Ts - std::min<uint64_t>(ctl->Ts, c->h_ctl->iter);
-                batch = (int)std::max<uint64_t>(1, std::min<uint64_t>(left, 64));
-            }
-            c->enqueue_steps(batch);
+            bt.last = bt.next(hctl(g).iter, secs());
+            g_enqueue_steps(g, bt.last);
         };
+        double tb = secs();
         if (!term) next_batch();
         while (!term) {
-            c->download_ctl();
-            c->raise_device_status();
-            Ctl& h = *c->h_ctl;
+            Ctl& h = g_download(g);
+            bt.measured(bt.last, secs() - tb);
             term = h.terminate;
             int due = h.pause & mode_mask;
             const double t = secs();
@@ -1325,91 +1725,67 @@ int osc_run_dumps(OscCtx* c, const OscStepControl* ctl, const OscDumpGates* gate
                 for (int m = 0; m < 2; ++m) {
                     if (!(due >> m & 1)) continue;
                     mark_t[m] = t;
-                    h.mark_r[m] = h.r;  // (already moved by the device for its own gates)
-                    h.mark_iter[m] = h.iter;
                     take_dump(m + 1, meta);
                 }
-                h.pause = 0;
-                CUDA_OK(cudaMemcpyAsync(c->ctl_cur(), c->h_ctl, sizeof(Ctl), cudaMemcpyHostToDevice, c->stream));
+                for (OscCtx* c : R) {  // (every rank paused identically)
+                    use(c);
+                    Ctl& hc = *c->h_ctl;
+                    for (int m = 0; m < 2; ++m)
+                        if (due >> m & 1) {
+                            hc.mark_r[m] = hc.r;  // (already moved by the device for its own gates)
+                            hc.mark_iter[m] = hc.iter;
+                        }
+                    hc.pause = 0;
+                    CUDA_OK(cudaMemcpyAsync(c->ctl_cur(), c->h_ctl, sizeof(Ctl), cudaMemcpyHostToDevice, c->stream));
+                }
             }
             if (!term && ctl->Tn > 0.0 && secs() >= ctl->Tn) term = 3;
             // keep the device busy while the host delivers finished dumps
+            tb = secs();
             if (!term) next_batch();
             deliver(false, -1);
         }
         deliver(true, -1);
         for (Pending& p : slot)
-            if (p.done) cudaEventDestroy(p.done);
-        double nd = 0.0;
-        osc_max_norm_dev(c, &nd);
-        const Ctl& h = *c->h_ctl;
-        out->final_r = h.r;
-        out->iterations = h.iter - ctl->iter;
-        out->accepted = h.accepted;
-        out->rejected = h.rejected;
-        out->wall_s = secs();
-        out->phase_hamiltonian_s = 0.0;
-        out->phase_evolve_s = out->wall_s - t_io;
-        out->phase_io_s = t_io;
-        out->max_worker_wait_s = 0.0;
-        out->final_max_norm_dev = nd;
-        out->termination = term == 2 ? 2 : (term == 3 ? 3 : 1);
+            for (cudaEvent_t e : p.done)
+                if (e) cudaEventDestroy(e);
+        fill_summary(g, ctl, term, secs(), t_io, out);
     });
 }
 
-int osc_run(OscCtx* c, const OscStepControl* ctl, osc_hook_fn hook, void* user, OscRunSummary* out) {
+int osc_run(OscCtx* g, const OscStepControl* ctl, osc_hook_fn hook, void* user, OscRunSummary* out) {
     return guarded([&] {
         using Clock = std::chrono::steady_clock;
         if (!ctl || !out) throw Error(OSC_ERR_CONFIG, "osc_run: null argument");
-        CUDA_OK(cudaSetDevice(c->device));
         const auto t0 = Clock::now();
         auto secs = [&] { return std::chrono::duration<double>(Clock::now() - t0).count(); };
-        c->begin(*ctl, 1);
+        g_begin(g, *ctl, 1);
         double t_io = 0.0;
-        int term = c->h_ctl->terminate;
+        int term = hctl(g).terminate;
         std::vector<double> host_state;
         uint64_t last_acc = 0;
+        Batcher bt{ctl};
         // batch size: one step at a time when a hook must see every accepted
         // state, else graph batches with a host check between batches
         while (!term) {
-            if (hook) {
-                c->enqueue_steps(1);
-            } else {
-                int batch = 64;
-                if (ctl->Ts > 0) {
-                    const uint64_t left = ctl->Ts - std::min<uint64_t>(ctl->Ts, c->h_ctl->iter);
-                    batch = (int)std::max<uint64_t>(1, std::min<uint64_t>(left, 64));
-                }
-                c->enqueue_steps(batch);
-            }
-            c->download_ctl();
-            c->raise_device_status();
-            term = c->h_ctl->terminate;
-            if (hook && c->h_ctl->accepted != last_acc) {
-                last_acc = c->h_ctl->accepted;
+            const double tb = secs();
+            bt.last = hook ? 1 : bt.next(hctl(g).iter, tb);
+            g_enqueue_steps(g, bt.last);
+            const Ctl& h = g_download(g);
+            bt.measured(bt.last, secs() - tb);
+            term = h.terminate;
+            if (hook && h.accepted != last_acc) {
+                last_acc = h.accepted;
                 const auto ti = Clock::now();
-                host_state.resize((size_t)c->ncell * c->nplanes);
-                get_state_impl(c, host_state.data(), host_state.size(), cudaMemcpyDeviceToHost);
-                OscHookInfo info{c->h_ctl->iter, c->h_ctl->r, c->h_ctl->dr, secs()};
+                host_state.resize(total_doubles(g));
+                get_state_impl(g, host_state.data(), host_state.size(), cudaMemcpyDeviceToHost);
+                OscHookInfo info{h.iter, h.r, h.dr, secs()};
                 hook(user, &info, host_state.data(), host_state.size());
                 t_io += std::chrono::duration<double>(Clock::now() - ti).count();
             }
             if (!term && ctl->Tn > 0.0 && secs() >= ctl->Tn) term = 3;
         }
-        double nd = 0.0;
-        osc_max_norm_dev(c, &nd);
-        const Ctl& h = *c->h_ctl;
-        out->final_r = h.r;
-        out->iterations = h.iter - ctl->iter;
-        out->accepted = h.accepted;
-        out->rejected = h.rejected;
-        out->wall_s = secs();
-        out->phase_hamiltonian_s = 0.0;
-        out->phase_evolve_s = out->wall_s - t_io;
-        out->phase_io_s = t_io;
-        out->max_worker_wait_s = 0.0;
-        out->final_max_norm_dev = nd;
-        out->termination = term == 2 ? 2 : (term == 3 ? 3 : 1);
+        fill_summary(g, ctl, term, secs(), t_io, out);
     });
 }
 

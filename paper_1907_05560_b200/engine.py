@@ -196,6 +196,30 @@ class Engine:
         check(lib().osc_local_range(self._ctx, C.byref(lo), C.byref(hi), C.byref(n)))
         self.t_lo, self.t_hi, self.state_doubles = lo.value, hi.value, n.value
         self.rank, self.nranks = rank, nranks
+        self.ordered = False
+
+    @classmethod
+    def group(cls, env: Environment, nranks: int, devices=None, ordered: bool = False) -> "Engine":
+        """Engine(env, lanes) over ``nranks`` GPUs in this process
+        (osc_create_group): theta blocks by make_partitions, one context per
+        rank, driven through one handle whose state() covers every
+        trajectory.  ``devices`` lists the GPU of each rank (default q mod
+        the device count); ranks sharing a GPU (or ``ordered=True``) use the
+        stream-ordered exchange, distinct GPUs the device-initiated one."""
+        self = cls.__new__(cls)
+        self.env = env
+        self._idbuf = None
+        self._ctx = C.c_void_p()
+        dev = (C.c_int * nranks)(*devices) if devices is not None else None
+        check(lib().osc_create_group(C.byref(env.desc), nranks, dev, native.GROUP_ORDERED if ordered else 0,
+                                     C.byref(self._ctx)))
+        lo, hi, n = C.c_int(), C.c_int(), C.c_size_t()
+        check(lib().osc_local_range(self._ctx, C.byref(lo), C.byref(hi), C.byref(n)))
+        self.t_lo, self.t_hi, self.state_doubles = lo.value, hi.value, n.value
+        nr, od = C.c_int(), C.c_int()
+        check(lib().osc_group_info(self._ctx, C.byref(nr), C.byref(od)))
+        self.rank, self.nranks, self.ordered = 0, nr.value, bool(od.value)
+        return self
 
     def close(self):
         if getattr(self, "_ctx", None):
@@ -356,6 +380,12 @@ class Engine:
     def launch_count(self) -> int:
         """Kernels this engine has launched so far (graph nodes included)."""
         return int(lib().osc_launch_count(self._ctx))
+
+
+def device_count() -> int:
+    n = C.c_int()
+    check(lib().osc_device_count(C.byref(n)))
+    return n.value
 
 
 def fp64_peak(device: int = 0) -> float:

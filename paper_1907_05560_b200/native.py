@@ -31,6 +31,7 @@ class OscComm(C.Structure):
 
 
 COMM_FORCE_COLLECTIVES = 1
+GROUP_ORDERED = 1
 
 
 class OscStepControl(C.Structure):
@@ -88,6 +89,7 @@ SYMBOLS = [
     "osc_max_norm_dev", "osc_begin", "osc_enqueue_steps", "osc_query", "osc_synchronize",
     "osc_stream", "osc_launches_per_step", "osc_debug_sums", "osc_set_schedule", "osc_set_launch_mode", "osc_get_launch_mode", "osc_comm_export", "osc_comm_connect", "osc_launch_count",
     "osc_fp64_peak", "osc_profile_stages", "osc_debug_evolve_bin", "osc_debug_trace", "osc_env_build", "osc_env_desc", "osc_env_destroy", "osc_fermi_integral",
+    "osc_create_group", "osc_group_info", "osc_device_count",
 ]
 
 _lib = None
@@ -107,6 +109,9 @@ def lib() -> C.CDLL:
     L.osc_comm_unique_id.argtypes = [vp]
     L.osc_create.argtypes = [C.POINTER(OscDesc), C.POINTER(OscComm), C.POINTER(vp)]
     L.osc_destroy.argtypes = [vp]
+    L.osc_create_group.argtypes = [C.POINTER(OscDesc), C.c_int, C.POINTER(C.c_int), C.c_int, C.POINTER(vp)]
+    L.osc_group_info.argtypes = [vp, C.POINTER(C.c_int), C.POINTER(C.c_int)]
+    L.osc_device_count.argtypes = [C.POINTER(C.c_int)]
     L.osc_local_range.argtypes = [vp, C.POINTER(C.c_int), C.POINTER(C.c_int),
                                   C.POINTER(C.c_size_t)]
     L.osc_init_states.argtypes = [vp]

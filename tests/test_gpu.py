@@ -738,3 +738,29 @@ def test_evolve_bin_edge_paths_match_reference(path):
         z = np.linalg.norm(h, axis=1) == 0.0
         assert np.array_equal(got[z], psi[z])
         assert np.abs(np.linalg.norm(got, axis=1) - np.linalg.norm(psi, axis=1)).max() <= 4e-16
+
+
+@pytest.mark.parametrize("k", [15, 16])
+def test_stage_kernel_resume_is_bit_exact_with_multi_tile_chunks(k):
+    """Stage kernels with several tiles per block (1024 theta x 128 E): a
+    state restored after k steps (odd and even: S4 walks its chunk in
+    alternating directions and S1 must accumulate in the same order) and
+    stepped on is bit-identical to the uninterrupted run."""
+    cfg = baseline_config("configs0", Abins=1024, Ebins=128, R0=50, Rn=1e9, dr=5e-5, max_dr=5e-5, Ts=0)
+    env, a = make(cfg)
+    a.set_launch_mode(Engine.LAUNCH_STAGES)
+    ctl = StepControl.from_config(cfg)
+    a.begin(ctl)
+    a.enqueue_steps(k)
+    q = a.query()
+    x = a.state()
+    env2, b = make(cfg)
+    b.set_launch_mode(Engine.LAUNCH_STAGES)
+    b.set_state(x)
+    c2 = StepControl.from_config(cfg)
+    c2.r, c2.dr, c2.iter = q["r"], q["dr"], q["iter"]
+    b.begin(c2)
+    a.enqueue_steps(9)
+    b.enqueue_steps(9)
+    assert a.query()["iter"] == b.query()["iter"] == k + 9
+    assert np.array_equal(a.state(), b.state())
