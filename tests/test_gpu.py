@@ -764,3 +764,18 @@ def test_stage_kernel_resume_is_bit_exact_with_multi_tile_chunks(k):
     b.enqueue_steps(9)
     assert a.query()["iter"] == b.query()["iter"] == k + 9
     assert np.array_equal(a.state(), b.state())
+
+
+def test_walltime_limit_stops_within_a_step():
+    """Tn (StepControl wall-time limit, checked after every step by the
+    reference, solver.cpp:453): the graph batches shrink as Tn approaches, so
+    the run stops with termination 'walltime' at most a few steps past Tn."""
+    cfg = baseline_config("configs0", Abins=1024, Ebins=128, R0=50, Rn=1e9, dr=5e-5, max_dr=5e-5, Ts=0)
+    env, eng = make(cfg)
+    eng.set_launch_mode(Engine.LAUNCH_STAGES)
+    ctl = StepControl.from_config(cfg)
+    ctl.Tn = 0.25
+    s = eng.run(ctl)
+    assert s.termination == "walltime"
+    assert 0.25 <= s.wall_s <= 0.25 + 0.01, s.wall_s
+    assert s.iterations > 100
