@@ -76,24 +76,7 @@ __device__ __forceinline__ bool res_finish(double* part, unsigned* bar, unsigned
     ++phase;
     __syncthreads();
     if (S.stop) return false;
-    double fv[NV];
-    double fm = 0.0;
-#pragma unroll
-    for (int k = 0; k < NV; ++k) fv[k] = 0.0;
-    for (int b = tid; b < (int)gridDim.x; b += kBlock) {
-        const double* p = slot + b;
-#pragma unroll
-        for (int k = 0; k < NV; ++k) fv[k] += __ldcg(p + (size_t)k * gridDim.x);
-        fm = fmax(fm, __ldcg(p + (size_t)NV * gridDim.x));
-    }
-    __syncthreads();  // S.red reuse
-    block_reduce<NV>(fv, fm, S.red);
-    if (tid == 0) {
-#pragma unroll
-        for (int k = 0; k < NV; ++k) out[k] = fv[k];
-        out[NV] = fm;
-    }
-    __syncthreads();
+    cols_reduce<NV>(slot, (int)gridDim.x, out);
     return true;
 }
 template <int NV>
@@ -173,9 +156,51 @@ __global__ void __launch_bounds__(kBlock, 1)
     const int tr0 = n ? (int)div_e(c0, a.e_magic, a.e_shift) : 0;
     const int ntr = n ? (int)div_e(c1 - 1, a.e_magic, a.e_shift) - tr0 + 1 : 0;
     unsigned phase = 0;
+    // sums0 of the loaded psi0 at r (S1), formed as S4 below forms the
+    // next-step moments and reduced by the same all-reduce: a restored state
+    // (set_state / resume_from) starts from the bits an uninterrupted run has
+    for (int i = tid; i < ntr; i += kBlock) {
+        const int traj = tr0 + i;
+        const Geo G = traj_geom<MODEL>(a, a.t_lo + traj / a.P, traj % a.P, S.c.r);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) rec[i].fold[0][j] = G.f[j];
+    }
     __syncthreads();
+    bool started = true;
+    {
+        double acc[NM];
+#pragma unroll
+        for (int k = 0; k < NM; ++k) acc[k] = 0.0;
+        for (int k = tid; k < n; k += kBlock) {
+            const int cell = c0 + k;
+            const int traj = (int)div_e(cell, a.e_magic, a.e_shift);
+            const int e = cell - traj * a.E;
+            CellK K;
+            K.v11 = ktab[e];
+            K.v12 = ktab[a.E + e];
+#pragma unroll
+            for (int s = 0; s < 4; ++s) {
+                K.g[s] = ktab[(2 + s) * a.E + e];
+                K.g2[s] = K.g[s] + K.g[s];
+            }
+            double x[4][4];
+#pragma unroll
+            for (int s = 0; s < 4; ++s)
+#pragma unroll
+                for (int c = 0; c < 4; ++c) x[s][c] = buf[0][(size_t)(s * 4 + c) * ch + k];
+            double B[2][3], Rr[3];
+            class_bloch(x, K, B);
+            bloch_sum(B, Rr);
+            fold_acc<NM>(acc, Rr, rec[traj - tr0].fold[0]);
+        }
+        if (nsteps > 0) {
+            started = res_allreduce<NM>(acc, 0.0, part, bar, phase, S, S.fin);
+            if (started && tid < NM) S.tot0[tid] = S.fin[tid];
+            __syncthreads();
+        }
+    }
 
-    for (int step = 0; step < nsteps; ++step) {
+    for (int step = 0; started && step < nsteps; ++step) {
         if (S.c.terminate | S.c.status | S.c.pause) break;
         const double r = S.c.r, dr = S.c.dr;
         const double rk[3] = {r, r + 0.5 * dr, r + dr};

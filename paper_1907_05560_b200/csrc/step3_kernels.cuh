@@ -401,26 +401,9 @@ __global__ void __launch_bounds__(kBlock, OSC3_MIN_BLOCKS) k_stage3(StepArgs a) 
     __syncthreads();
     if (!is_last) return;
     __threadfence();
-    double fv[NV];
-    double fm = 0.0;
-#pragma unroll
-    for (int k = 0; k < NV; ++k) fv[k] = 0.0;
-    for (int b = tid; b < (int)gridDim.x; b += kBlock) {
-        const double* p = a.partials + b;
-#pragma unroll
-        for (int k = 0; k < NV; ++k) fv[k] += __ldcg(p + (size_t)k * gridDim.x);
-        fm = fmax(fm, __ldcg(p + (size_t)NV * gridDim.x));
-    }
-    __syncthreads();
-    block_reduce<NV>(fv, fm, red);
     __shared__ double fin[2 * kNM3Max + 1];
     __shared__ double pub[kSlotDoubles];
-    if (tid == 0) {
-#pragma unroll
-        for (int k = 0; k < NV; ++k) fin[k] = fv[k];
-        fin[NV] = fm;
-    }
-    __syncthreads();
+    cols_reduce<NV>(a.partials, (int)gridDim.x, fin);
     if (tid < kSlotDoubles) {
         // slot layout: per set 36 doubles (9 x up to 4 geometric moments),
         // S2 = sums1 | sums2, S4 error at index 36

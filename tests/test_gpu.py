@@ -779,3 +779,29 @@ def test_walltime_limit_stops_within_a_step():
     assert s.termination == "walltime"
     assert 0.25 <= s.wall_s <= 0.25 + 0.01, s.wall_s
     assert s.iterations > 100
+
+
+def test_resident_kernel_resume_is_bit_exact():
+    """Resident kernel (configs[0] shape, 173 cells per block): 24 steps in one
+    launch end on the same bits as 15 steps, a restore of that state into a
+    fresh engine and 9 more steps — the kernel forms the restored state's
+    sums0 as its S4 forms the next-step moments and reduces them with the same
+    all-reduce."""
+    cfg = baseline_config("configs0", R0=50, Rn=1e9, dr=5e-5, max_dr=5e-5, Ts=0)
+    ctl = StepControl.from_config(cfg)
+    env, a = make(cfg)
+    assert a.launch_mode == Engine.LAUNCH_RESIDENT
+    a.begin(ctl)
+    a.enqueue_steps(24)
+    _, a2 = make(cfg)
+    a2.begin(ctl)
+    a2.enqueue_steps(15)
+    q = a2.query()
+    _, b = make(cfg)
+    b.set_state(a2.state())
+    c2 = StepControl.from_config(cfg)
+    c2.r, c2.dr, c2.iter = q["r"], q["dr"], q["iter"]
+    b.begin(c2)
+    b.enqueue_steps(9)
+    assert a.query()["iter"] == b.query()["iter"] == 24
+    assert np.array_equal(a.state(), b.state())
