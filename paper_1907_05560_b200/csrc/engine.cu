@@ -300,7 +300,7 @@ struct OscCtx {
         cudaLaunchConfig_t cfg{};
         cfg.gridDim = dim3((nflav == 2 && (stage == 2 || stage == 3)) ? nblocks23 : nblocks);
         cfg.blockDim = dim3(kBlock);
-        cfg.dynamicSmemBytes = nflav == 3 ? stage3_smem_bytes(ntr_max) : stage_smem_bytes(stage, schedule, ntr_max, E, rec_stride);
+        cfg.dynamicSmemBytes = nflav == 3 ? stage3_smem_bytes(ntr_max, stage) : stage_smem_bytes(stage, schedule, ntr_max, E, rec_stride);
         cfg.stream = stream;
         cudaLaunchAttribute attr[1];
         attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -688,7 +688,7 @@ int osc_create(const OscDesc* desc, const OscComm* comm, OscCtx** out) {
                 c->ntr_max = chunk / c->E + 2;
                 size_t smax = 0;
                 if (c->nflav == 3) {
-                    smax = stage3_smem_bytes(c->ntr_max);
+                    smax = stage3_smem_bytes(c->ntr_max, 4);
                 } else {
                     // padded record stride where two blocks per SM still fit, else compact
                     // (env OSC_REC_COMPACT=1 forces the compact stride: tests)
@@ -824,7 +824,7 @@ int osc_create(const OscDesc* desc, const OscComm* comm, OscCtx** out) {
         a.e_magic = c->e_magic;
         a.e_shift = c->e_shift;
         a.schedule = c->schedule;
-        c->stash.alloc((size_t)c->npad * c->nplanes);
+        c->stash.alloc((size_t)c->npad * (c->nflav == 3 ? kSt3Planes : c->nplanes));
         a.Rnu = desc->Rnu;
         a.dcos2 = 1.0 / c->T;
         a.phi_measure = desc->model >= OSC_MODEL_EXT_BULB ? 1.0 / c->P : 1.0;
@@ -1318,7 +1318,7 @@ int osc_set_schedule(OscCtx* g, int schedule) {
         if (schedule != 0 && schedule != 1) throw Error(OSC_ERR_CONFIG, "schedule must be 0 or 1");
         for (OscCtx* c : ranks_of(g)) {
             use(c);
-            if (schedule == 1 && !c->stash.p) c->stash.alloc((size_t)c->npad * c->nplanes);
+            if (schedule == 1 && !c->stash.p) c->stash.alloc((size_t)c->npad * (c->nflav == 3 ? kSt3Planes : c->nplanes));
             c->schedule = schedule;
             c->args.schedule = schedule;
             c->args.stash = c->stash.p;

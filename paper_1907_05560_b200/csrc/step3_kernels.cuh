@@ -19,6 +19,11 @@
 namespace oscb200 {
 
 constexpr int kNM3Max = 18;  // 9 x (a, b): single-angle and bulb geometries
+// stash planes (schedule 1): [0, 36) mid (S2) -> half2 (S3, in place) in the
+// state plane order, [36, 72) Uf = exp(-i H0 dl2) of each class (S2 -> S4,
+// 3x3 complex row-major, re/im)
+constexpr int kSt3Uf = 36;
+constexpr int kSt3Planes = 72;
 
 #ifndef OSC3_MIN_BLOCKS
 #define OSC3_MIN_BLOCKS 1  // resident 3-flavour blocks per SM the register budget targets
@@ -129,8 +134,13 @@ __device__ __forceinline__ void cr_control3(const StepArgs& a, StageShared& S, b
 }
 
 #ifndef OSC3_S4_OOL
-#define OSC3_S4_OOL 1
+#define OSC3_S4_OOL 0  // (S4 evaluates two exponentials since U1 and half2 come from the stash)
 #endif
+__host__ __device__ constexpr int stage3_pf_planes(int stage) { return stage == 4 ? 36 : 18; }
+__host__ __device__ constexpr size_t stage3_rec_bytes(int ntr_max) { return ((size_t)ntr_max * sizeof(TrajRec3) + 15) & ~(size_t)15; }
+__device__ __forceinline__ void cp_async8_ca(void* dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
 __device__ __noinline__ Mat3 exp_herm3_ool(const Herm3& H, double tau) { return exp_herm3(H, tau); }
 
 template <int MODEL, int STAGE>
@@ -257,15 +267,40 @@ __global__ void __launch_bounds__(kBlock, OSC3_MIN_BLOCKS) k_stage3(StepArgs a) 
     double emax = 0.0;
     const bool stash = a.schedule == 1;
 
-    for (int cell = c0 + tid; cell < c1; cell += kBlock) {
+    // Streamed operands of the next cell are copied into this thread's
+    // shared-memory column while the current cell's exponentials run
+    // (cp.async, double-buffered): one block of 8 warps per SM (255
+    // registers) cannot hide their latency otherwise, and in registers they
+    // would spill.  Slots [0, 18): psi0 of the class (S3 with the stash: mid
+    // = Um psi0 from S2), [18, 36) (S4 with the stash): half2 from S3.
+    constexpr int PF = stage3_pf_planes(STAGE);
+    double* pf = reinterpret_cast<double*>(dsm3 + stage3_rec_bytes(a.ntr_max));
+    const double* src0 = (STAGE == 3 && stash) ? a.stash : psi0;
+    auto issue = [&](int cl, int buf) {
+        if (cl < c1) {
+#pragma unroll
+            for (int j = 0; j < PF; ++j) {
+                if (j >= 18 && !stash) break;
+                const double* sp = (j < 18 ? src0 : a.stash) + (size_t)((2 * ((j % 18) / 6) + pc) * 6 + j % 6) * np;
+                cp_async8_ca(pf + ((size_t)buf * PF + j) * kBlock + tid, sp + cl);
+            }
+        }
+        cp_async_commit();
+    };
+    issue(c0 + tid, 0);
+    int it = 0;
+    for (int cell = c0 + tid; cell < c1; cell += kBlock, ++it) {
         const int traj = (int)div_e(cell, a.e_magic, a.e_shift);
         const int e = cell - traj * a.E;
         const TrajRec3& R = rec[traj - tr0];
+        cp_async_wait_all();  // this thread's copies of this cell
+        issue(cell + kBlock, (it + 1) & 1);
+        const double* cur_pf = pf + (size_t)(it & 1) * PF * kBlock + tid;
         double x[3][6];
 #pragma unroll
         for (int f = 0; f < 3; ++f)
 #pragma unroll
-            for (int c = 0; c < 6; ++c) x[f][c] = __ldg(psi0 + (size_t)((2 * f + pc) * 6 + c) * np + cell);
+            for (int c = 0; c < 6; ++c) x[f][c] = cur_pf[(size_t)(f * 6 + c) * kBlock];
         double g[3];
 #pragma unroll
         for (int f = 0; f < 3; ++f) g[f] = __ldg(a.g + (size_t)(2 * f + pc) * a.E + e);
@@ -298,6 +333,21 @@ __global__ void __launch_bounds__(kBlock, OSC3_MIN_BLOCKS) k_stage3(StepArgs a) 
             for (int j = 0; j < NG; ++j)
 #pragma unroll
                 for (int k = 0; k < 9; ++k) acc[NM + 9 * j + k] += R.fold[1][j] * Rr[k];
+            if (stash) {
+                // S3 continues from mid, S4 averages with full1's propagator:
+                // neither recomputes an exponential of H0
+#pragma unroll
+                for (int f = 0; f < 3; ++f)
+#pragma unroll
+                    for (int c = 0; c < 6; ++c) __stcg(a.stash + (size_t)((2 * f + pc) * 6 + c) * np + cell, y[f][c]);
+#pragma unroll
+                for (int i = 0; i < 3; ++i)
+#pragma unroll
+                    for (int j = 0; j < 3; ++j) {
+                        __stcg(a.stash + (size_t)(kSt3Uf + pc * 18 + (i * 3 + j) * 2) * np + cell, uf.m[i][j].re);
+                        __stcg(a.stash + (size_t)(kSt3Uf + pc * 18 + (i * 3 + j) * 2 + 1) * np + cell, uf.m[i][j].im);
+                    }
+            }
 #pragma unroll
             for (int f = 0; f < 3; ++f) apply3(uf, x[f], y[f]);
             weighted_rho3(y, g, pc, Rr);
@@ -306,12 +356,19 @@ __global__ void __launch_bounds__(kBlock, OSC3_MIN_BLOCKS) k_stage3(StepArgs a) 
 #pragma unroll
                 for (int k = 0; k < 9; ++k) acc[9 * j + k] += R.fold[0][j] * Rr[k];
         } else if (STAGE == 3) {
-            const Mat3 um = prop(0, 0), uh = prop(2, 1);
+            const Mat3 uh = prop(2, 1);
+            Mat3 um;
+            if (!stash) um = prop(0, 0);
             double hh[3][6];
 #pragma unroll
             for (int f = 0; f < 3; ++f) {
                 double mid[6];
-                apply3(um, x[f], mid);
+                if (stash) {  // mid = Um psi0 from S2 (prefetched); half2 replaces it in place
+#pragma unroll
+                    for (int c = 0; c < 6; ++c) mid[c] = x[f][c];
+                } else {
+                    apply3(um, x[f], mid);
+                }
                 apply3(uh, mid, hh[f]);
                 if (stash)
 #pragma unroll
@@ -323,31 +380,35 @@ __global__ void __launch_bounds__(kBlock, OSC3_MIN_BLOCKS) k_stage3(StepArgs a) 
 #pragma unroll
                 for (int k = 0; k < 9; ++k) acc[9 * j + k] += R.fold[0][j] * Rr[k];
         } else {
-            double h2[3][6];
-            if (stash) {
-#pragma unroll
-                for (int f = 0; f < 3; ++f)
-#pragma unroll
-                    for (int c = 0; c < 6; ++c) h2[f][c] = __ldcg(a.stash + (size_t)((2 * f + pc) * 6 + c) * np + cell);
-            } else {
-                const Mat3 um = prop(0, 0), uh = prop(2, 1);
-#pragma unroll
-                for (int f = 0; f < 3; ++f) {
-                    double mid[6];
-                    apply3(um, x[f], mid);
-                    apply3(uh, mid, h2[f]);
-                }
-            }
+            // (the exponentials first: with the out-of-line copy everything
+            // live across a call goes to the stack)
             const Mat3 u3 = prop(3, 2);
             double out[3][6];
+            {
+                double h2[3][6];
+                if (stash) {  // (prefetched)
 #pragma unroll
-            for (int f = 0; f < 3; ++f) {
-                double f3[6];
-                apply3(u3, x[f], f3);
+                    for (int f = 0; f < 3; ++f)
 #pragma unroll
-                for (int c = 0; c < 6; ++c) {
-                    out[f][c] = (h2[f][c] + f3[c]) * 0.5;  // evolve_avg, beam.cpp:188-218
-                    res[(size_t)((2 * f + pc) * 6 + c) * np + cell] = out[f][c];
+                        for (int c = 0; c < 6; ++c) h2[f][c] = cur_pf[(size_t)(18 + f * 6 + c) * kBlock];
+                } else {
+                    const Mat3 um = prop(0, 0), uh = prop(2, 1);
+#pragma unroll
+                    for (int f = 0; f < 3; ++f) {
+                        double mid[6];
+                        apply3(um, x[f], mid);
+                        apply3(uh, mid, h2[f]);
+                    }
+                }
+#pragma unroll
+                for (int f = 0; f < 3; ++f) {
+                    double f3[6];
+                    apply3(u3, x[f], f3);
+#pragma unroll
+                    for (int c = 0; c < 6; ++c) {
+                        out[f][c] = (h2[f][c] + f3[c]) * 0.5;  // evolve_avg, beam.cpp:188-218
+                        res[(size_t)((2 * f + pc) * 6 + c) * np + cell] = out[f][c];
+                    }
                 }
             }
             weighted_rho3(out, g, pc, Rr);
@@ -356,16 +417,25 @@ __global__ void __launch_bounds__(kBlock, OSC3_MIN_BLOCKS) k_stage3(StepArgs a) 
 #pragma unroll
                 for (int k = 0; k < 9; ++k) acc[9 * j + k] += R.fold[0][j] * Rr[k];
             // avgA = (full1 + full2)/2 = Q psi0 with Q = (U1 + U2)/2: one
-            // 3x3 apply per species for the error instead of two
-            Mat3 Q = prop(0, 2);
-            {
-                const Mat3 u2 = prop(1, 2);
+            // 3x3 apply per species for the error instead of two; U1 comes
+            // from S2 (stash) or is recomputed
+            const Mat3 u2 = prop(1, 2);
+            Mat3 Q;
+            if (stash) {
 #pragma unroll
                 for (int i = 0; i < 3; ++i)
 #pragma unroll
                     for (int j = 0; j < 3; ++j)
-                        Q.m[i][j] = Cx{(Q.m[i][j].re + u2.m[i][j].re) * 0.5, (Q.m[i][j].im + u2.m[i][j].im) * 0.5};
+                        Q.m[i][j] = Cx{__ldcg(a.stash + (size_t)(kSt3Uf + pc * 18 + (i * 3 + j) * 2) * np + cell),
+                                       __ldcg(a.stash + (size_t)(kSt3Uf + pc * 18 + (i * 3 + j) * 2 + 1) * np + cell)};
+            } else {
+                Q = prop(0, 2);
             }
+#pragma unroll
+            for (int i = 0; i < 3; ++i)
+#pragma unroll
+                for (int j = 0; j < 3; ++j)
+                    Q.m[i][j] = Cx{(Q.m[i][j].re + u2.m[i][j].re) * 0.5, (Q.m[i][j].im + u2.m[i][j].im) * 0.5};
 #pragma unroll
             for (int f = 0; f < 3; ++f) {
                 double av[6];
@@ -435,7 +505,11 @@ __global__ void __launch_bounds__(kBlock, OSC3_MIN_BLOCKS) k_stage3(StepArgs a) 
     }
 }
 
-inline size_t stage3_smem_bytes(int ntr_max) { return (size_t)ntr_max * sizeof(TrajRec3); }
+// Dynamic shared memory of a 3-flavour stage: trajectory records, then the
+// double-buffered per-thread prefetch columns.
+inline size_t stage3_smem_bytes(int ntr_max, int stage) {
+    return stage3_rec_bytes(ntr_max) + (size_t)2 * stage3_pf_planes(stage) * kBlock * sizeof(double);
+}
 
 // Single GPU: the control update of a batch's last step (one block).
 template <int MODEL>
