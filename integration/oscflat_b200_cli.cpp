@@ -2,8 +2,9 @@
 // (tools/oscflat.cpp:122-165 cmd_run, option wiring :245-319) over the B200
 // drop-in Engine (solver_b200.cpp), with snapshot dumps gated on the device.
 //
-//   oscflat_b200 run    -c CONFIG [-o DIR] [--override k=v]... [--lanes N] [--gpus N] [-v]
-//   oscflat_b200 resume -c CONFIG -s SNAPSHOT [same options]
+//   oscflat_b200 run     -c CONFIG [-o DIR] [--override k=v]... [--lanes N] [--gpus N] [-v]
+//   oscflat_b200 resume  -c CONFIG -s SNAPSHOT [same options]
+//   oscflat_b200 analyze -i SNAPSHOT [-o DIR] [--what survival|spectra|content|all]
 //
 // Same flow and outputs as the reference: parse + overrides, require_runnable,
 // config hash, Environment / StepControl from the config, Engine(env, lanes),
@@ -31,6 +32,7 @@
 #include <string>
 #include <vector>
 
+#include "oscflat/analysis.hpp"
 #include "oscflat/config.hpp"
 #include "oscflat/parallel.hpp"
 #include "oscflat/snapshot.hpp"
@@ -50,6 +52,7 @@ constexpr int kExitIo = 4;
 struct Options {
     std::string command;
     std::string config_path, snapshot_path, output_dir = ".";
+    std::string input_path, what = "all";  // analyze
     std::vector<std::string> overrides;
     int lanes = 0;  // 0: the config's
     int gpus = 0;   // 0: every visible device
@@ -58,7 +61,8 @@ struct Options {
 
 [[noreturn]] void usage(const char* argv0) {
     std::cerr << "usage: " << argv0
-              << " run|resume -c CONFIG [-s SNAPSHOT] [-o DIR] [--override key=value]... [--lanes N] [--gpus N] [-v]\n";
+              << " run|resume -c CONFIG [-s SNAPSHOT] [-o DIR] [--override key=value]... [--lanes N] [--gpus N] [-v]\n"
+              << "       " << argv0 << " analyze -i SNAPSHOT [-o DIR] [--what survival|spectra|content|all]\n";
     std::exit(kExitConfig);
 }
 
@@ -66,7 +70,7 @@ Options parse_args(int argc, char** argv) {
     Options o;
     if (argc < 2) usage(argv[0]);
     o.command = argv[1];
-    if (o.command != "run" && o.command != "resume") usage(argv[0]);
+    if (o.command != "run" && o.command != "resume" && o.command != "analyze") usage(argv[0]);
     for (int i = 2; i < argc; ++i) {
         const std::string a = argv[i];
         auto value = [&]() -> std::string {
@@ -80,7 +84,13 @@ Options parse_args(int argc, char** argv) {
         else if (a == "--lanes") o.lanes = std::stoi(value());
         else if (a == "--gpus") o.gpus = std::stoi(value());
         else if (a == "-v" || a == "--verbose") o.verbose = true;
+        else if (a == "-i" || a == "--input") o.input_path = value();
+        else if (a == "--what") o.what = value();
         else throw ConfigError("unknown option " + a);
+    }
+    if (o.command == "analyze") {
+        if (o.input_path.empty()) throw ConfigError("analyze needs --input");
+        return o;
     }
     if (o.config_path.empty()) throw ConfigError("--config is required");
     if (o.command == "resume" && o.snapshot_path.empty()) throw ConfigError("resume needs --snapshot");
@@ -207,11 +217,20 @@ int cmd_run(const Options& opt) {
     return 0;
 }
 
+// `analyze` (tools/oscflat.cpp:334-339): the reference's own post-processing
+// (analysis::analyze_file, host code, unchanged) on snapshots the GPU wrote.
+int cmd_analyze(const Options& opt) {
+    for (const auto& f : analysis::analyze_file(opt.input_path, opt.output_dir, opt.what))
+        std::cout << "wrote " << f << "\n";
+    return 0;
+}
+
 }  // namespace
 
 int main(int argc, char** argv) {
     try {
-        return cmd_run(parse_args(argc, argv));
+        const Options opt = parse_args(argc, argv);
+        return opt.command == "analyze" ? cmd_analyze(opt) : cmd_run(opt);
     } catch (const ConfigError& e) {
         std::cerr << "config error: " << e.what() << "\n";
         return kExitConfig;

@@ -4,8 +4,8 @@
   cases, compiled unchanged against the drop-in Engine with a doctest
   stand-in: integration/_build/test_solver_b200), on one GPU and with the
   Engine spread over two ranks;
-* the run/resume CLI (integration/oscflat_b200_cli.cpp; tools/oscflat.cpp
-  cmd_run) with device-gated dumps through the reference's WriterLane /
+* the run/resume/analyze CLI (integration/oscflat_b200_cli.cpp;
+  tools/oscflat.cpp cmd_run, analyze) with device-gated dumps through the reference's WriterLane /
   SnapshotFileWriter, compared file by file with the same CLI source driving
   the unmodified reference engine (integration/_build/oscflat_ref_cli), and
   run -> dump -> resume bit-exactness at the configs[2] size.
@@ -129,6 +129,26 @@ def test_cli_run_and_resume_match_reference_cli(tmp_path):
         runs[tag + "_resume"] = _run(exe, path, d, "resume", "-s", str(tmp_path / "ref" / snap))
     assert runs["gpu_resume"]["iterations"] == runs["ref_resume"]["iterations"]
     _compare_dirs(tmp_path / "gpu_resume", tmp_path / "ref_resume", 40)
+    # `analyze` (the reference's analysis::analyze_file, host code) on the
+    # last mode-1 and mode-2 files each engine wrote: survival grids, final
+    # spectra and the content series agree
+    for kind in ("Snapshot", "Average"):
+        last = sorted((f for f in _files(tmp_path / "ref") if kind in f),
+                      key=lambda f: int(f.split(kind)[1].split("_")[0]))[-1]
+        outs = []
+        for tag, exe in (("gpu", CLI), ("ref", REF_CLI)):
+            od = tmp_path / f"an_{tag}_{kind}"
+            r = subprocess.run([exe, "analyze", "-i", str(tmp_path / tag / last), "-o", str(od)], capture_output=True,
+                               text=True, timeout=300)
+            assert r.returncode == 0, r.stdout + r.stderr
+            outs.append(od)
+        names = sorted(os.listdir(outs[0]))
+        assert names == sorted(os.listdir(outs[1])) and len(names) == (8 if kind == "Snapshot" else 1)
+        for n in names:
+            a = np.loadtxt(outs[0] / n, delimiter=",", skiprows=1, ndmin=2)
+            b = np.loadtxt(outs[1] / n, delimiter=",", skiprows=1, ndmin=2)
+            assert a.shape == b.shape and a.size > 0, n
+            assert np.allclose(a, b, rtol=1e-8, atol=1e-10), (n, np.max(np.abs(a - b)))
 
 
 def test_cli_resume_is_bit_exact_at_configs2_size(tmp_path):
