@@ -1,5 +1,5 @@
 """Device time per step of one BASELINE config at full size (quick A/B).
-usage: python tools/time_config.py configs1 [steps] [launch]"""
+usage: python tools/time_config.py configs1 [steps] [launch|-] [schedule]"""
 import sys
 
 import torch
@@ -12,8 +12,10 @@ steps = int(sys.argv[2]) if len(sys.argv) > 2 else 200
 cfg = baseline_config(name)
 env = Environment.from_config(cfg)
 eng = Engine(env)
-if len(sys.argv) > 3:
+if len(sys.argv) > 3 and sys.argv[3] != "-":
     eng.set_launch_mode(int(sys.argv[3]))
+if len(sys.argv) > 4:
+    eng.set_schedule(int(sys.argv[4]))
 eng.init_states()
 ctl = StepControl.from_config(cfg)
 ctl.Rn, ctl.Ts = 1e9, 0
