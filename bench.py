@@ -266,6 +266,13 @@ def main():
     ctl_e2e = StepControl.from_config(cfg)
     ctl_e2e.Ts = e2e_steps
     ctl_e2e.Rn = 1e9
+    # warm-up of the end-to-end path (untimed, as the W device steps): the
+    # first transfers through freshly pinned buffers run at ~half the link
+    # rate while their pages are mapped
+    for _ in range(max(1, min(a.warmup, 2))):
+        eng.set_state_host_ptr(host_in.data_ptr(), n)
+        eng.run(ctl_e2e)
+        eng.get_state_host_ptr(host_out.data_ptr(), n)
     barrier()
     f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     t0 = time.perf_counter()
