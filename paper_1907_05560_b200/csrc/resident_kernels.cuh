@@ -55,18 +55,19 @@ __device__ __forceinline__ bool res_wait(const unsigned* bar, unsigned target) {
 // -> part[phase & 1][value][block] -> release arrival.  res_finish: acquire
 // wait -> every block sums all partials in the same fixed order ->
 // out[0..NV] = totals, max.
+// Block partial (block_cols_store, step_kernels.cuh) into
+// part[phase & 1][value][block], then the release arrival.
 template <int NV>
 __device__ __forceinline__ void res_arrive(double (&v)[NV], double mx, double* part, unsigned* bar,
-                                           unsigned phase, ResShared& S) {
-    block_reduce<NV>(v, mx, S.red);
-    if (threadIdx.x == 0) {  // [value][block] layout: the reads coalesce
-        double* p = part + (size_t)(phase & 1) * gridDim.x * kSlotDoubles + blockIdx.x;
-#pragma unroll
-        for (int k = 0; k < NV; ++k) p[(size_t)k * gridDim.x] = v[k];
-        p[(size_t)NV * gridDim.x] = mx;
-        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
-    }
+                                           unsigned phase, ResShared& S, double* scratch) {
+    block_cols_store<NV>(v, mx, scratch, part + (size_t)(phase & 1) * gridDim.x * kSlotDoubles + blockIdx.x,
+                         gridDim.x);
+    // (the barrier ending block_cols_store orders every column's store before
+    // thread 0's release: the cooperative-groups grid sync pattern)
+    if (threadIdx.x == 0) asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
+    (void)S;
 }
+
 template <int NV>
 __device__ __forceinline__ bool res_finish(double* part, unsigned* bar, unsigned& phase, ResShared& S,
                                            double* out) {
@@ -81,8 +82,8 @@ __device__ __forceinline__ bool res_finish(double* part, unsigned* bar, unsigned
 }
 template <int NV>
 __device__ __forceinline__ bool res_allreduce(double (&v)[NV], double mx, double* part, unsigned* bar,
-                                              unsigned& phase, ResShared& S, double* out) {
-    res_arrive<NV>(v, mx, part, bar, phase, S);
+                                              unsigned& phase, ResShared& S, double* out, double* scratch) {
+    res_arrive<NV>(v, mx, part, bar, phase, S, scratch);
     return res_finish<NV>(part, bar, phase, S, out);
 }
 
@@ -91,9 +92,10 @@ __device__ __forceinline__ bool res_allreduce(double (&v)[NV], double mx, double
 constexpr int kResProps = 24;
 
 // Shared-memory bytes of the resident kernel for a chunk of `ch` cells.
+constexpr int kResScratch = kResMaxNV * kBlock;  // all-reduce transposition scratch (doubles)
 inline size_t resident_smem_bytes(int ch, int ntr_max, int E) {
     return (size_t)(2 * kPlanes + kResProps) * ch * sizeof(double) + (size_t)ntr_max * sizeof(TrajRec) +
-           (size_t)6 * E * sizeof(double);
+           (size_t)6 * E * sizeof(double) + (size_t)kResScratch * sizeof(double);
 }
 
 // nsteps evolution steps with the state resident in shared memory.
@@ -130,6 +132,7 @@ __global__ void __launch_bounds__(kBlock, 1)
                         pst[(size_t)(row + 4 * c + 2) * ch + k], pst[(size_t)(row + 4 * c + 3) * ch + k]};
     };
     double* ktab = reinterpret_cast<double*>(rec + ntr_cap);
+    double* scratch = ktab + 6 * a.E;  // [kResMaxNV][kBlock] (res_arrive)
 
     grid_dependency_wait();
     if (tid == 0) {
@@ -194,7 +197,7 @@ __global__ void __launch_bounds__(kBlock, 1)
             fold_acc<NM>(acc, Rr, rec[traj - tr0].fold[0]);
         }
         if (nsteps > 0) {
-            started = res_allreduce<NM>(acc, 0.0, part, bar, phase, S, S.fin);
+            started = res_allreduce<NM>(acc, 0.0, part, bar, phase, S, S.fin, scratch);
             if (started && tid < NM) S.tot0[tid] = S.fin[tid];
             __syncthreads();
         }
@@ -277,7 +280,7 @@ __global__ void __launch_bounds__(kBlock, 1)
                 put(0, k, um);
                 put(8, k, uf);
             }
-            if (!res_allreduce<2 * NM>(acc, 0.0, part, bar, phase, S, S.fin)) break;
+            if (!res_allreduce<2 * NM>(acc, 0.0, part, bar, phase, S, S.fin, scratch)) break;
             if (tid < 2 * NM) S.tot1[tid] = S.fin[tid];
         }
         // H1 (sums1, r+dr) and H2 (sums2, r+dr/2)
@@ -317,7 +320,7 @@ __global__ void __launch_bounds__(kBlock, 1)
                 fold_acc<NM>(acc, Rr, R->fold[0]);
                 put(16, k, P);
             }
-            res_arrive<NM>(acc, 0.0, part, bar, phase, S);
+            res_arrive<NM>(acc, 0.0, part, bar, phase, S, scratch);
             for (int k = tid; k < n; k += kBlock) {
                 CellK K;
                 double x[4][4];
@@ -392,7 +395,7 @@ __global__ void __launch_bounds__(kBlock, 1)
                 bloch_sum(B, Rr);
                 fold_acc<NM>(acc, Rr, R->fold[0]);
             }
-            if (!res_allreduce<NM>(acc, emax, part, bar, phase, S, S.fin)) break;
+            if (!res_allreduce<NM>(acc, emax, part, bar, phase, S, S.fin, scratch)) break;
             if (tid <= NM) S.totn[tid] = S.fin[tid];
         }
 

@@ -2,6 +2,7 @@
 // block per SM, N all-reduces of NV doubles; variants of the arrival/wait.
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cuda_runtime.h>
 #include "../paper_1907_05560_b200/csrc/resident_kernels.cuh"
 using namespace oscb200;
@@ -9,6 +10,7 @@ using namespace oscb200;
 template <int NV, int VAR>
 __global__ void __launch_bounds__(kBlock, 1) k_probe(int n, double* part, unsigned* bar, double* out) {
     __shared__ ResShared S;
+    extern __shared__ double scratch[];
     unsigned phase = 0;
     double acc = threadIdx.x * 1e-3;
     for (int i = 0; i < n; ++i) {
@@ -16,7 +18,7 @@ __global__ void __launch_bounds__(kBlock, 1) k_probe(int n, double* part, unsign
 #pragma unroll
         for (int k = 0; k < NV; ++k) v[k] = acc + k;
         if (VAR == 0) {
-            if (!res_allreduce<NV>(v, acc, part, bar, phase, S, S.fin)) break;
+            if (!res_allreduce<NV>(v, acc, part, bar, phase, S, S.fin, scratch)) break;
         } else if (VAR == 2) {  // write partial + barrier, no read
             block_reduce<NV>(v, acc, S.red);
             double* slot = part + (size_t)(phase & 1) * gridDim.x * kSlotDoubles;
@@ -176,7 +178,9 @@ void run(int nsm, const char* name) {
     for (int rep = 0; rep < 3; ++rep) {
         cudaMemset(bar, 0, 4);
         cudaEventRecord(e0);
-        cudaLaunchCooperativeKernel((void*)k_probe<NV, VAR>, nsm, kBlock, args, 0, 0);
+        const size_t sm = (size_t)kResScratch * sizeof(double);
+        cudaFuncSetAttribute(k_probe<NV, VAR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        cudaLaunchCooperativeKernel((void*)k_probe<NV, VAR>, nsm, kBlock, args, sm, 0);
         cudaEventRecord(e1);
         cudaEventSynchronize(e1);
         float ms; cudaEventElapsedTime(&ms, e0, e1);
@@ -185,8 +189,10 @@ void run(int nsm, const char* name) {
     }
 }
 
-int main() {
+int main(int argc, char** argv) {
     int nsm; cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
+    if (argc > 1) nsm = std::atoi(argv[1]);  // grid size (blocks, one per SM)
+    printf("grid %d\n", nsm);
     run<12, 1>(nsm, "counter barrier only");
     run<12, 2>(nsm, "block reduce+write+barrier");
     run<12, 3>(nsm, "barrier+read+reduce");
