@@ -447,23 +447,13 @@ __global__ void __launch_bounds__(kBlock, OSC3_MIN_BLOCKS) k_stage3(StepArgs a) 
     }
     grid_launch_dependents();
 
-    block_reduce<NV>(acc, emax, red);
-    if (a.cr3 && (STAGE == 2 || STAGE == 3 || STAGE == 4)) {  // reduced by every block of S3 / S4 / next S2
-        if (tid == 0) {
-            double* p = a.cpart[Tr::slot] + blockIdx.x;
-#pragma unroll
-            for (int k = 0; k < NV; ++k) p[(size_t)k * gridDim.x] = acc[k];
-            p[(size_t)NV * gridDim.x] = emax;
-        }
-        return;
-    }
+    // block partial by transposition through the prefetch columns (free
+    // now; sized for NV + 1 columns), stored [value][block] (a reducer's
+    // loads of one value across blocks coalesce)
+    const bool cr_out = a.cr3 && (STAGE == 2 || STAGE == 3 || STAGE == 4);  // reduced by every block of S3 / S4 / next S2
+    block_cols_store<NV>(acc, emax, pf, (cr_out ? a.cpart[Tr::slot] : a.partials) + blockIdx.x, gridDim.x);
+    if (cr_out) return;
     if (tid == 0) {
-        // partials are stored [value][block]: the last block's loads of one
-        // value across blocks coalesce (one request per 32 blocks)
-        double* p = a.partials + blockIdx.x;
-#pragma unroll
-        for (int k = 0; k < NV; ++k) p[(size_t)k * gridDim.x] = acc[k];
-        p[(size_t)NV * gridDim.x] = emax;
         __threadfence();
         const unsigned ticket = atomicAdd(&a.ctl->counter[Tr::slot], 1u);
         is_last = ticket == gridDim.x - 1;
@@ -508,7 +498,9 @@ __global__ void __launch_bounds__(kBlock, OSC3_MIN_BLOCKS) k_stage3(StepArgs a) 
 // Dynamic shared memory of a 3-flavour stage: trajectory records, then the
 // double-buffered per-thread prefetch columns.
 inline size_t stage3_smem_bytes(int ntr_max, int stage) {
-    return stage3_rec_bytes(ntr_max) + (size_t)2 * stage3_pf_planes(stage) * kBlock * sizeof(double);
+    // (the columns double as the block-partial scratch: 2 x 18 moments + max in S2)
+    const int cols = std::max(2 * stage3_pf_planes(stage), 2 * kNM3Max + 1);
+    return stage3_rec_bytes(ntr_max) + (size_t)cols * kBlock * sizeof(double);
 }
 
 // Single GPU: the control update of a batch's last step (one block).
