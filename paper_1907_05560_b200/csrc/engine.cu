@@ -691,9 +691,13 @@ int osc_create(const OscDesc* desc, const OscComm* comm, OscCtx** out) {
                     smax = stage3_smem_bytes(c->ntr_max, 4);
                 } else {
                     // padded record stride where two blocks per SM still fit, else compact
-                    // (env OSC_REC_COMPACT=1 forces the compact stride: tests)
+                    // (env OSC_REC_COMPACT=1 forces the compact stride: tests).  Models
+                    // 2-4 (four geometric moments) spill a few registers at the two-
+                    // blocks-per-SM budget: the compact stride leaves L1 more room for
+                    // them (configs[3]: 129.9 -> 125.4 us/step; configs[2], model 1,
+                    // no spills: padded 118.0 vs compact 118.9)
                     const char* rc_env = std::getenv("OSC_REC_COMPACT");
-                    const bool force_compact = rc_env && std::atoi(rc_env) == 1;
+                    const bool force_compact = (rc_env && std::atoi(rc_env) == 1) || desc->model >= OSC_MODEL_EXT_BULB;
                     for (int stride : {kRecStridePadded, 0}) {
                         if (force_compact && stride) continue;
                         smax = 0;
