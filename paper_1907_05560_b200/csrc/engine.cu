@@ -272,6 +272,7 @@ struct OscCtx {
         for (double*& p : pinned)
             if (p) cudaFreeHost(p);
         if (!kids.empty()) return;  // (a group handle owns no device buffers)
+        cudaSetDevice(device);  // (a group's ranks live on several devices)
         drop_graphs();
         if (comm) {
             try {
