@@ -233,6 +233,7 @@ struct OscCtx {
     int ordered = 0;
     bool in_group = false;  // (a rank of a group: the group drives its exchange)
     std::vector<cudaEvent_t> gev;
+    std::vector<cudaEvent_t> xev;  // chunked host transfers (set/get_state)
 
     DevBuf<double> cos2, sin0, cphi, sphi, vac11, vac12, g, ktab_g;
     DevBuf<double> cpart[4];  // single GPU: block partials of S2, S3, S4 (consumer-side reduction)
@@ -273,6 +274,7 @@ struct OscCtx {
             if (p) cudaFreeHost(p);
         if (!kids.empty()) return;  // (a group handle owns no device buffers)
         cudaSetDevice(device);  // (a group's ranks live on several devices)
+        for (cudaEvent_t e : xev) cudaEventDestroy(e);
         drop_graphs();
         if (comm) {
             try {
@@ -1024,13 +1026,54 @@ void g_sync(OscCtx* g) {
     }
 }
 
+// Host transfers of the mode-1 payload in chunks of whole trajectories on the
+// copy stream, each chunk's (un)packing on the compute stream overlapping
+// the next chunk's copy (cross-stream events); the compute stream ends
+// ordered after the last copy.
+constexpr int kXferChunks = 8;
+void ensure_xfer(OscCtx* c) {
+    if (!c->copy_stream) CUDA_OK(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+    while ((int)c->xev.size() < kXferChunks + 1) {
+        cudaEvent_t e;
+        CUDA_OK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        c->xev.push_back(e);
+    }
+}
+// element range of chunk k (whole trajectories)
+void xfer_chunk(const OscCtx* c, int k, size_t& i0, size_t& i1) {
+    const size_t per_traj = (size_t)c->E * c->nplanes;
+    const size_t tpc = ((size_t)c->ntraj + kXferChunks - 1) / kXferChunks;
+    i0 = std::min((size_t)c->ntraj, tpc * k) * per_traj;
+    i1 = std::min((size_t)c->ntraj, tpc * (k + 1)) * per_traj;
+}
+bool chunked(const OscCtx* c, cudaMemcpyKind kind) {
+    return kind != cudaMemcpyDeviceToDevice && kind != cudaMemcpyDefault && local_doubles(c) >= ((size_t)1 << 20) &&
+           c->ntraj >= kXferChunks;
+}
+
 void set_state_local(OscCtx* c, const double* src, cudaMemcpyKind kind) {
     const size_t want = local_doubles(c);
     use(c);
     if (c->staging.n < want) c->staging.alloc(want);
-    CUDA_OK(cudaMemcpyAsync(c->staging.p, src, want * sizeof(double), kind, c->stream));
-    k_unpack<<<c->nsm * 8, 256, 0, c->stream>>>(c->args, c->staging.p, want);
-    c->count();
+    if (chunked(c, kind)) {
+        ensure_xfer(c);
+        CUDA_OK(cudaEventRecord(c->xev[kXferChunks], c->stream));  // staging free
+        CUDA_OK(cudaStreamWaitEvent(c->copy_stream, c->xev[kXferChunks], 0));
+        for (int k = 0; k < kXferChunks; ++k) {
+            size_t i0, i1;
+            xfer_chunk(c, k, i0, i1);
+            if (i1 <= i0) continue;
+            CUDA_OK(cudaMemcpyAsync(c->staging.p + i0, src + i0, (i1 - i0) * sizeof(double), kind, c->copy_stream));
+            CUDA_OK(cudaEventRecord(c->xev[k], c->copy_stream));
+            CUDA_OK(cudaStreamWaitEvent(c->stream, c->xev[k], 0));
+            k_unpack<<<c->nsm * 8, 256, 0, c->stream>>>(c->args, c->staging.p, i0, i1);
+            c->count();
+        }
+    } else {
+        CUDA_OK(cudaMemcpyAsync(c->staging.p, src, want * sizeof(double), kind, c->stream));
+        k_unpack<<<c->nsm * 8, 256, 0, c->stream>>>(c->args, c->staging.p, 0, want);
+        c->count();
+    }
     CUDA_OK(cudaGetLastError());
     c->bloch_stale = true;
 }
@@ -1039,10 +1082,27 @@ void get_state_local(OscCtx* c, double* dst, cudaMemcpyKind kind) {
     const size_t want = local_doubles(c);
     use(c);
     if (c->staging.n < want) c->staging.alloc(want);
-    k_pack<<<c->nsm * 8, 256, 0, c->stream>>>(c->args, c->staging.p, want);
-    c->count();
+    if (chunked(c, kind)) {
+        ensure_xfer(c);
+        for (int k = 0; k < kXferChunks; ++k) {
+            size_t i0, i1;
+            xfer_chunk(c, k, i0, i1);
+            if (i1 <= i0) continue;
+            k_pack<<<c->nsm * 8, 256, 0, c->stream>>>(c->args, c->staging.p, i0, i1);
+            c->count();
+            CUDA_OK(cudaEventRecord(c->xev[k], c->stream));
+            CUDA_OK(cudaStreamWaitEvent(c->copy_stream, c->xev[k], 0));
+            CUDA_OK(cudaMemcpyAsync(dst + i0, c->staging.p + i0, (i1 - i0) * sizeof(double), kind, c->copy_stream));
+        }
+        CUDA_OK(cudaEventRecord(c->xev[kXferChunks], c->copy_stream));
+        CUDA_OK(cudaStreamWaitEvent(c->stream, c->xev[kXferChunks], 0));
+    } else {
+        k_pack<<<c->nsm * 8, 256, 0, c->stream>>>(c->args, c->staging.p, 0, want);
+        c->count();
+        CUDA_OK(cudaGetLastError());
+        CUDA_OK(cudaMemcpyAsync(dst, c->staging.p, want * sizeof(double), kind, c->stream));
+    }
     CUDA_OK(cudaGetLastError());
-    CUDA_OK(cudaMemcpyAsync(dst, c->staging.p, want * sizeof(double), kind, c->stream));
 }
 
 // Whole payloads: the ranks' theta blocks are contiguous and in rank order,
@@ -1680,7 +1740,7 @@ int osc_run_dumps(OscCtx* g, const OscStepControl* ctl, const OscDumpGates* gate
                 if (mode == 1) {
                     double* st = k == 0 ? c->staging.p : c->staging2.p;
                     len = local_doubles(c);
-                    k_pack<<<c->nsm * 8, 256, 0, c->stream>>>(c->args, st, len);
+                    k_pack<<<c->nsm * 8, 256, 0, c->stream>>>(c->args, st, 0, len);
                     c->count();
                     CUDA_OK(cudaGetLastError());
                     src = st;
