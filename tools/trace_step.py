@@ -19,7 +19,7 @@ from paper_1907_05560_b200 import Engine, Environment, StepControl, baseline_con
 from paper_1907_05560_b200.native import lib  # noqa: E402
 
 name = sys.argv[1] if len(sys.argv) > 1 else "configs2"
-cfg = baseline_config(name)
+cfg = baseline_config(name, **({"Abins": int(os.environ["TRACE_ABINS"])} if os.environ.get("TRACE_ABINS") else {}))
 env = Environment.from_config(cfg)
 eng = Engine(env)
 eng.set_launch_mode(Engine.LAUNCH_STAGES)
