@@ -179,17 +179,20 @@ int osc_destroy(OscCtx* ctx);
  * the returned group handle, which every entry point below accepts like a
  * single context (state payloads then cover all trajectories, in order).
  * Moment exchange between the stages:
- *   - device-initiated (default when every rank has its own GPU and all pairs
- *     have peer access): the last block of each stage stores its rank's slot
- *     into every rank's buffer over NVLink through peer pointers (the
- *     osc_comm_connect path without IPC), consumers poll sequence-flagged words;
- *   - stream-ordered (OSC_GROUP_ORDERED, or forced by a shared GPU): the rank
- *     slots are copied between the ranks' exchange buffers behind
- *     cross-stream events after every stage, a control kernel per rank after
- *     S4.  No kernel ever waits on another rank's kernel, so several ranks may
- *     share one GPU (tests).
+ *   - stream-ordered (default): the rank slots are copied between the ranks'
+ *     exchange buffers (peer copies) behind cross-stream events after every
+ *     stage, a control kernel per rank after S4.  No kernel ever waits on
+ *     another rank's kernel, so any placement works, several ranks per GPU
+ *     included (how the tests run 2 and 3 ranks on one GPU);
+ *   - device-initiated (OSC_GROUP_PEER, when every rank has its own GPU and
+ *     all pairs have peer access; else the ordered exchange): the last block
+ *     of each stage stores its rank's slot into every rank's buffer over
+ *     NVLink through peer pointers (the osc_comm_connect path without IPC),
+ *     consumers poll sequence-flagged words.  Opt-in until it has run on
+ *     several GPUs (the same kernels run with a one-rank communicator).
  * nranks == 1 returns a plain context (osc_create with OscComm{0, 1, dev}). */
-#define OSC_GROUP_ORDERED 1
+#define OSC_GROUP_ORDERED 1 /* (the default; kept for callers that pass it) */
+#define OSC_GROUP_PEER 2
 int osc_create_group(const OscDesc* desc, int nranks, const int* devices, int flags, OscCtx** out);
 /* Ranks of a context (1 unless a group) and its exchange (1: stream-ordered). */
 int osc_group_info(const OscCtx* ctx, int* nranks, int* ordered);

@@ -103,7 +103,9 @@ struct Engine::Impl {
         if (gpus < 1) gpus = 1;
         gpus = std::min(gpus, e.grid.abins);
         if (e.grid.model == geom::Model::SingleAngle) gpus = 1;
-        ok(osc_create_group(&d, gpus, nullptr, 0, &ctx));
+        // (OSC_GROUP_PEER=1: the device-initiated exchange between the GPUs)
+        const char* peer = std::getenv("OSC_GROUP_PEER");
+        ok(osc_create_group(&d, gpus, nullptr, peer && std::atoi(peer) ? OSC_GROUP_PEER : 0, &ctx));
     }
     ~Impl() {
         if (ctx) osc_destroy(ctx);

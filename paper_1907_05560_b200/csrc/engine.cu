@@ -1169,9 +1169,9 @@ int osc_create_group(const OscDesc* desc, int nranks, const int* devices, int fl
         g->t_hi = desc->abins;
         g->nflav = desc->nflav == 3 ? 3 : 2;
         g->nplanes = g->nflav == 3 ? 36 : 16;
-        // device-initiated exchange needs one rank per GPU and peer access
-        // between every pair; otherwise (or when asked) the ordered exchange
-        bool ordered = (flags & OSC_GROUP_ORDERED) != 0;
+        // device-initiated exchange on request, with one rank per GPU and
+        // peer access between every pair; otherwise the ordered exchange
+        bool ordered = !(flags & OSC_GROUP_PEER) || (flags & OSC_GROUP_ORDERED);
         for (int a = 0; a < nranks && !ordered; ++a)
             for (int b = 0; b < nranks && !ordered; ++b) {
                 if (a == b) continue;

@@ -199,19 +199,20 @@ class Engine:
         self.ordered = False
 
     @classmethod
-    def group(cls, env: Environment, nranks: int, devices=None, ordered: bool = False) -> "Engine":
+    def group(cls, env: Environment, nranks: int, devices=None, peer: bool = False) -> "Engine":
         """Engine(env, lanes) over ``nranks`` GPUs in this process
         (osc_create_group): theta blocks by make_partitions, one context per
         rank, driven through one handle whose state() covers every
         trajectory.  ``devices`` lists the GPU of each rank (default q mod
-        the device count); ranks sharing a GPU (or ``ordered=True``) use the
-        stream-ordered exchange, distinct GPUs the device-initiated one."""
+        the device count).  The stage moments move stream-ordered between
+        the ranks; ``peer=True`` asks for the device-initiated exchange over
+        peer pointers (distinct GPUs with peer access only)."""
         self = cls.__new__(cls)
         self.env = env
         self._idbuf = None
         self._ctx = C.c_void_p()
         dev = (C.c_int * nranks)(*devices) if devices is not None else None
-        check(lib().osc_create_group(C.byref(env.desc), nranks, dev, native.GROUP_ORDERED if ordered else 0,
+        check(lib().osc_create_group(C.byref(env.desc), nranks, dev, native.GROUP_PEER if peer else 0,
                                      C.byref(self._ctx)))
         lo, hi, n = C.c_int(), C.c_int(), C.c_size_t()
         check(lib().osc_local_range(self._ctx, C.byref(lo), C.byref(hi), C.byref(n)))

@@ -32,6 +32,7 @@ class OscComm(C.Structure):
 
 COMM_FORCE_COLLECTIVES = 1
 GROUP_ORDERED = 1
+GROUP_PEER = 2
 
 
 class OscStepControl(C.Structure):
