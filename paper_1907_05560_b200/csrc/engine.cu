@@ -489,6 +489,7 @@ struct OscCtx {
         h.pend = 0;
         h.dump_mask = 0;  // snapshot gates are armed by osc_run_dumps only
         h.pause = 0;
+        h.nstep += 1;  // (exchange tags never repeat across runs)
         h.commit = commit;
         h.dr_max = c.dr_max;
         h.dr_min = c.dr_min;
@@ -506,6 +507,8 @@ struct OscCtx {
         upload_ctl();
     }
 };
+
+static void enable_mr_cr(OscCtx* c);
 
 namespace {
 
@@ -762,7 +765,7 @@ int osc_create(const OscDesc* desc, const OscComm* comm, OscCtx** out) {
                 c->cpart[k].alloc((size_t)c->nblocks * (2 * kNM3Max + 1));
                 CUDA_OK(cudaMemset(c->cpart[k].p, 0, c->cpart[k].n * sizeof(double)));
             }
-        if (!c->coll && c->nflav == 2)
+        if (c->nflav == 2)  // (multi-rank contexts reduce consumer-side once the peers are connected)
             for (int k = 1; k < 4; ++k) {
                 c->cpart[k].alloc((size_t)std::max(c->nblocks, c->nblocks23) * (2 * 12 + 1));
                 CUDA_OK(cudaMemset(c->cpart[k].p, 0, c->cpart[k].n * sizeof(double)));
@@ -1215,6 +1218,7 @@ int osc_create_group(const OscDesc* desc, int nranks, const int* devices, int fl
             for (OscCtx* k : g->kids) {
                 for (int q = 0; q < nranks; ++q) k->args.peer_xll[q] = g->kids[q]->xll.p;
                 k->args.p2p = 1;
+                enable_mr_cr(k);
                 k->drop_graphs();
             }
         }
@@ -1304,6 +1308,7 @@ int osc_trial_step_error(OscCtx* c, double r, double dr, double* err) {
                 for (OscCtx* k : c->kids) {
                     use(k);
                     k->enqueue_step();
+                    k->finalize();
                 }
             }
         }
@@ -1423,6 +1428,20 @@ int osc_comm_export(OscCtx* c, void* out128) {
     });
 }
 
+}  // extern "C"
+
+// Device-initiated exchange connected: 2-flavour contexts switch to the
+// consumer-side reduction with the S2-side control (as on one GPU; the rank
+// totals travel tagged 4 nstep + slot, step_kernels.cuh mr_totals).  Env
+// OSC_MR_CR=0 keeps the last-block publish per stage and the control fused
+// into S4's last block.
+static void enable_mr_cr(OscCtx* c) {
+    const char* env = std::getenv("OSC_MR_CR");
+    c->args.cr = (c->nflav == 2 && OSC_CR && !(env && std::atoi(env) == 0)) ? 1 : 0;
+}
+
+extern "C" {
+
 int osc_comm_connect(OscCtx* c, const void* handles) {
     return guarded([&] {
         if (!c->coll) throw Error(OSC_ERR_CONFIG, "osc_comm_connect: not a multi-rank context");
@@ -1443,6 +1462,7 @@ int osc_comm_connect(OscCtx* c, const void* handles) {
             a.peer_xll[q] = static_cast<unsigned long long*>(pb);
         }
         a.p2p = 1;
+        enable_mr_cr(c);
         c->drop_graphs();  // kernel arguments changed
     });
 }

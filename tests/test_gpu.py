@@ -805,3 +805,30 @@ def test_resident_kernel_resume_is_bit_exact():
     b.enqueue_steps(9)
     assert a.query()["iter"] == b.query()["iter"] == 24
     assert np.array_equal(a.state(), b.state())
+
+
+def test_collective_p2p_dumps_and_trial_match_fused_path():
+    """The multi-rank consumer-side exchange (device-initiated, a one-rank
+    communicator: every tagged slot published and polled) under device-gated
+    dumps — pauses mid-batch, k_finalize per batch — and a trial step: the
+    same dump sequence and bits as the fused single-GPU path."""
+    cfg = baseline_config("configs0", Abins=24, Ebins=20, R0=50, Rn=50.2, dr=1e-3, max_dr=0.05, eps0=1e-8, Ts=60)
+    gates = [(0.0, 0.0, 5), (0.002, 0.0, 0)]
+    out = []
+    for coll in (False, True):
+        env = Environment.from_config(cfg)
+        eng = Engine(env, force_collectives=coll)
+        eng.init_states()
+        if coll:
+            eng.comm_connect([eng.comm_export()])
+        else:
+            eng.set_launch_mode(Engine.LAUNCH_STAGES)
+        got = []
+        s = eng.run_dumps(StepControl.from_config(cfg), gates, 3, lambda m, meta, p: got.append((m, meta.iter, p)))
+        err = eng.trial_step_error(50.1, 0.01)
+        out.append((s.iterations, s.accepted, s.rejected, got, err, eng.state()))
+    (ia, aa, ra, ga, ea, sa), (ib, ab, rb, gb, eb, sb) = out
+    assert (ia, aa, ra) == (ib, ab, rb) and ia > 10 and len(ga) > 5
+    assert [(m, i) for m, i, _ in ga] == [(m, i) for m, i, _ in gb]
+    assert all(np.array_equal(pa, pb) for (_, _, pa), (_, _, pb) in zip(ga, gb))
+    assert ea == eb and np.array_equal(sa, sb)
