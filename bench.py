@@ -62,55 +62,120 @@ def _dist():
 
 # ------------------------------------------------------------------ clocks
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """SM clock and throttle reasons sampled DURING the timed regions.
 
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    NVML is polled from a thread of this process (about every 2 ms, so even a
+    20-step timed region of a few milliseconds is seen); `mark()` brackets the
+    timed regions on the host clock and only samples inside them count.  When
+    NVML cannot be loaded the sampler falls back to an `nvidia-smi -lms` child
+    process (slow to start: it may miss a short region, and says so)."""
+
+    REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
+               0x4: "sw_power_cap", 0x80: "hw_power_brake"}
 
     def __init__(self, device: int):
         self.device = device
-        self.proc = None
-        self.path = None
+        self.samples = []   # (t, sm_mhz, reasons bitmask)
+        self.windows = []   # (t0, t1) timed regions, host clock
+        self.max_mhz = None
+        self._stop = False
+        self._thread = None
+        self._nvml = None
+        self._smi = None
+        self._smi_path = None
+
+    def _handle(self):
+        import pynvml
+
+        pynvml.nvmlInit()
+        self._nvml = pynvml
+        try:
+            import torch
+
+            uuid = str(torch.cuda.get_device_properties(self.device).uuid)
+            if not uuid.startswith("GPU-"):
+                uuid = "GPU-" + uuid
+            return pynvml.nvmlDeviceGetHandleByUUID(uuid)
+        except Exception:  # noqa: BLE001
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES", "")
+            ids = [v for v in vis.split(",") if v.strip().isdigit()]
+            idx = int(ids[self.device]) if self.device < len(ids) else self.device
+            return pynvml.nvmlDeviceGetHandleByIndex(idx)
+
+    def _poll(self, h):
+        nv = self._nvml
+        while not self._stop:
+            try:
+                mhz = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                try:
+                    rs = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                except Exception:  # noqa: BLE001
+                    rs = nv.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+                self.samples.append((time.perf_counter(), float(mhz), int(rs)))
+            except Exception:  # noqa: BLE001
+                pass
+            time.sleep(0.002)
 
     def start(self):
-        fd, self.path = tempfile.mkstemp(prefix="clocks_", suffix=".csv")
-        os.close(fd)
+        import threading
+
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.Q}",
-                 "--format=csv,noheader,nounits", "-lms", "50"],
-                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+            h = self._handle()
+            self.max_mhz = float(self._nvml.nvmlDeviceGetMaxClockInfo(h, self._nvml.NVML_CLOCK_SM))
+            self._thread = threading.Thread(target=self._poll, args=(h,), daemon=True)
+            self._thread.start()
+            return
+        except Exception:  # noqa: BLE001
+            self._nvml = None
+        fd, self._smi_path = tempfile.mkstemp(prefix="clocks_", suffix=".csv")
+        os.close(fd)
+        q = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self._smi = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.device}", f"--query-gpu={q}",
+                 "--format=csv,noheader,nounits", "-lms", "20"],
+                stdout=open(self._smi_path, "w"), stderr=subprocess.DEVNULL)
         except OSError:
-            self.proc = None
+            self._smi = None
+
+    def mark(self, t0: float, t1: float):
+        self.windows.append((t0, t1))
 
     def stop(self) -> dict:
-        if self.proc is None:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        time.sleep(0.12)
-        self.proc.terminate()
+        if self._thread is not None:
+            self._stop = True
+            self._thread.join(timeout=2)
+            inside = [s for s in self.samples if any(a <= s[0] <= b for a, b in self.windows)]
+            bits = 0
+            for s in inside:
+                bits |= s[2]
+            reasons = sorted(n for b, n in self.REASONS.items() if bits & b)
+            sm = [s[1] for s in inside]
+            return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": self.max_mhz,
+                    "reasons": reasons, "samples": len(inside),
+                    "source": "NVML polled in-process every ~2 ms; samples inside the timed regions "
+                              "(device-resident steps and the end-to-end call)"}
+        if self._smi is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        time.sleep(0.1)
+        self._smi.terminate()
         try:
-            self.proc.wait(timeout=5)
+            self._smi.wait(timeout=5)
         except subprocess.TimeoutExpired:
-            self.proc.kill()
-        rows = []
-        for line in open(self.path):
-            parts = [p.strip() for p in line.split(",")]
-            if len(parts) < 9:
-                continue
-            try:
-                rows.append(parts)
-            except ValueError:
-                pass
-        os.unlink(self.path)
+            self._smi.kill()
+        rows = [[p.strip() for p in line.split(",")] for line in open(self._smi_path)]
+        rows = [r for r in rows if len(r) >= 7]
+        os.unlink(self._smi_path)
         sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
         mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({n for r in rows for n, v in zip(names, r[5:9]) if v.lower() == "active"})
-        busy = [s for s in sm if s > 0.5 * (max(sm) if sm else 1)]
+        reasons = sorted({n for r in rows for n, v in zip(names, r[3:7]) if v.lower() == "active"})
+        busy = [s for s in sm if s > 0.5 * max(sm)] if sm else []
         return {"sm_mhz": statistics.median(busy) if busy else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(rows)}
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(rows),
+                "source": "nvidia-smi -lms 20 over the whole run (NVML python binding unavailable)"}
 
 
 # --------------------------------------------------------------- reference
@@ -239,15 +304,16 @@ def main():
     barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     n_launch0 = eng.launch_count()
+    tw0 = time.perf_counter()
     e0.record(stream)
     eng.enqueue_steps(a.steps)
     e1.record(stream)
     n_launch = eng.launch_count() - n_launch0
     e1.synchronize()
+    sampler.mark(tw0, time.perf_counter())
     barrier()
     ms = max_over_ranks(e0.elapsed_time(e1))
     q = eng.query()
-    clocks = sampler.stop()
     if q["status"] != 0:
         raise SystemExit(f"device reported status {q['status']}")
     value = cells_total * a.steps / (ms * 1e-3)
@@ -283,6 +349,8 @@ def main():
     f1.record(stream)
     f1.synchronize()
     wall_e2e = time.perf_counter() - t0
+    sampler.mark(t0, t0 + wall_e2e)
+    clocks = sampler.stop()
     barrier()
     ms_e2e = max_over_ranks(max(f0.elapsed_time(f1), wall_e2e * 1e3))
     e2e_value = cells_total * summ.iterations / (ms_e2e * 1e-3)
