@@ -287,6 +287,12 @@ int osc_profile_stages(OscCtx* ctx, int nsteps, float* ms_out3);
  * kernels' branch-free chain with its fallback branch; 1: the safe path. */
 int osc_debug_evolve_bin(int device, size_t n, const double* h, const double* dl, const double* psi,
                          double* out, int path);
+/* exp(-i H tau) of 3x3 Hermitian matrices through the device code of the
+ * 3-flavour stages (csrc/su3_exp.cuh; generalises flavor::evolve_bin,
+ * beam.hpp:105-121, to configs[1]) for known-answer tests: H [n][9] packed
+ * (d0, d1, d2, re/im of h01, h02, h12), tau [n] -> U [n][18] row-major re/im.
+ * path 0: one-call exponential; 1: shared decomposition + phases (S2). */
+int osc_debug_exp3(int device, size_t n, const double* H, const double* tau, double* U, int path);
 /* Development: per-block %globaltimer stamps of the stage launches of four
  * iterations (layout in csrc/step_kernels.cuh, trace_mark); OSC_ERR_CONFIG
  * unless the library was built with -DOSC_TRACE. */

@@ -302,7 +302,7 @@ struct OscCtx {
         }
         cudaLaunchConfig_t cfg{};
         cfg.gridDim = dim3((nflav == 2 && (stage == 2 || stage == 3)) ? nblocks23 : nblocks);
-        cfg.blockDim = dim3(kBlock);
+        cfg.blockDim = dim3(nflav == 3 ? kBlock3 : kBlock);
         cfg.dynamicSmemBytes = nflav == 3 ? stage3_smem_bytes(ntr_max, stage) : stage_smem_bytes(stage, schedule, ntr_max, E, rec_stride);
         cfg.stream = stream;
         cudaLaunchAttribute attr[1];
@@ -320,7 +320,7 @@ struct OscCtx {
         if (!args.cr && !args.cr3) return;
         cudaLaunchConfig_t cfg{};
         cfg.gridDim = dim3(1);
-        cfg.blockDim = dim3(kBlock);
+        cfg.blockDim = dim3(args.cr3 ? kBlock3 : kBlock);
         cfg.stream = stream;
         cudaLaunchAttribute attr[1];
         attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -547,6 +547,26 @@ __global__ void k_debug_evolve(int n, const double* h, const double* dl, const d
     double y[4];
     apply(u[0], x, y);
     for (int k = 0; k < 4; ++k) out[4 * i + k] = y[k];
+}
+
+// exp(-i H tau) of 3x3 Hermitian matrices through the device code of the
+// 3-flavour stages (su3_exp.cuh): path 0 = exp_herm3, 1 = eig_herm3 +
+// exp_from_eig (S2's shared decomposition).  H [n][9] packed (d0 d1 d2, re/im
+// of h01, h02, h12), U [n][18] row-major re/im.
+__global__ void k_debug_exp3(int n, const double* H, const double* tau, double* U, int path) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    Herm3 h;
+    for (int k = 0; k < 3; ++k) h.d[k] = H[9 * i + k];
+    h.o01 = Cx{H[9 * i + 3], H[9 * i + 4]};
+    h.o02 = Cx{H[9 * i + 5], H[9 * i + 6]};
+    h.o12 = Cx{H[9 * i + 7], H[9 * i + 8]};
+    const Mat3 u = path == 0 ? exp_herm3(h, tau[i]) : exp_from_eig(eig_herm3(h), tau[i]);
+    for (int r = 0; r < 3; ++r)
+        for (int c = 0; c < 3; ++c) {
+            U[18 * i + (r * 3 + c) * 2] = u.m[r][c].re;
+            U[18 * i + (r * 3 + c) * 2 + 1] = u.m[r][c].im;
+        }
 }
 
 void validate(const OscDesc* d) {
@@ -1513,6 +1533,22 @@ int osc_debug_evolve_bin(int device, size_t n, const double* h, const double* dl
         k_debug_evolve<<<(unsigned)((n + 127) / 128), 128>>>((int)n, d, d + 3 * n, d + 4 * n, d + 8 * n, path);
         CUDA_OK(cudaGetLastError());
         CUDA_OK(cudaMemcpy(out, d + 8 * n, n * 4 * sizeof(double), cudaMemcpyDeviceToHost));
+    });
+}
+
+int osc_debug_exp3(int device, size_t n, const double* H, const double* tau, double* U, int path) {
+    return guarded([&] {
+        if (n == 0) return;
+        if (!H || !tau || !U) throw Error(OSC_ERR_CONFIG, "osc_debug_exp3: null argument");
+        CUDA_OK(cudaSetDevice(device));
+        double* d = nullptr;
+        CUDA_OK(cudaMalloc(&d, n * 28 * sizeof(double)));
+        std::unique_ptr<double, decltype(&cudaFree)> hold(d, &cudaFree);
+        CUDA_OK(cudaMemcpy(d, H, n * 9 * sizeof(double), cudaMemcpyHostToDevice));
+        CUDA_OK(cudaMemcpy(d + 9 * n, tau, n * sizeof(double), cudaMemcpyHostToDevice));
+        k_debug_exp3<<<(unsigned)((n + 127) / 128), 128>>>((int)n, d, d + 9 * n, d + 10 * n, path);
+        CUDA_OK(cudaGetLastError());
+        CUDA_OK(cudaMemcpy(U, d + 10 * n, n * 18 * sizeof(double), cudaMemcpyDeviceToHost));
     });
 }
 

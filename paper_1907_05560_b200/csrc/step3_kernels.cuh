@@ -28,6 +28,16 @@ constexpr int kSt3Planes = 72;
 #ifndef OSC3_MIN_BLOCKS
 #define OSC3_MIN_BLOCKS 1  // resident 3-flavour blocks per SM the register budget targets
 #endif
+#ifndef OSC3_BLOCK
+#define OSC3_BLOCK 256
+#endif
+// Threads per 3-flavour block (one block per SM).  The 3-flavour kernels are
+// latency-bound, so a block's time is its rounds of (class, cell) items per
+// thread times the latency of one item: configs[1] (2 x 65536 items over 148
+// SMs, 3.46 per thread at 256 threads) takes 4 rounds with 256 threads, 3 with
+// 320 (200 registers instead of 255).
+constexpr int kBlock3 = OSC3_BLOCK;
+constexpr int kWarps3 = kBlock3 / 32;
 
 struct TrajRec3 {
     double hb[4][9];   // beam part (H_nunu + matter) for H0..H3, particle convention
@@ -102,7 +112,7 @@ __device__ __forceinline__ void cr_control3(const StepArgs& a, StageShared& S, b
     for (int i = tid; i < kCtlWords; i += blockDim.x)
         reinterpret_cast<unsigned long long*>(&S.cs)[i] = __ldcg(reinterpret_cast<const unsigned long long*>(a.ctl) + i);
     const double x0 = tid < NM ? __ldcg(a.xbuf + tid) : 0.0;
-    cr_reduce<NM>(a.cpart[3], a.nblocks, S.red, S.fin);
+    cr_reduce<NM, kBlock3>(a.cpart[3], a.nblocks, S.red, S.fin);
     Ctl& c = S.cs;
     if (tid == 0) {
         S.accept = c.pend ? ctl_advance(&c, a, S.fin[NM], c.bad_sums == 0) : -1;
@@ -144,14 +154,14 @@ __device__ __forceinline__ void cp_async8_ca(void* dst, const void* src) {
 __device__ __noinline__ Mat3 exp_herm3_ool(const Herm3& H, double tau) { return exp_herm3(H, tau); }
 
 template <int MODEL, int STAGE>
-__global__ void __launch_bounds__(kBlock, OSC3_MIN_BLOCKS) k_stage3(StepArgs a) {
+__global__ void __launch_bounds__(kBlock3, OSC3_MIN_BLOCKS) k_stage3(StepArgs a) {
     using Tr = StageTraits<STAGE>;
     constexpr int NG = MODEL == 0 ? 1 : 2;  // geometric moments (a | a, b)
     constexpr int NM = 9 * NG;
     constexpr int NV = NM * Tr::nsets;
     extern __shared__ __align__(128) unsigned char dsm3[];
     __shared__ double tot[4][kNM3Max];
-    __shared__ double red[kWarps * (2 * kNM3Max + 1)];
+    __shared__ double red[kWarps3 * (2 * kNM3Max + 1)];
     __shared__ int is_last;
 
     const Ctl* ctl = a.ctl;
@@ -189,9 +199,9 @@ __global__ void __launch_bounds__(kBlock, OSC3_MIN_BLOCKS) k_stage3(StepArgs a) 
                               : 0.0;
         __shared__ double cfin[2 * kNM3Max + 1];
         if (STAGE == 3)
-            cr_reduce<2 * NM>(a.cpart[1], (int)gridDim.x, red, cfin);
+            cr_reduce<2 * NM, kBlock3>(a.cpart[1], (int)gridDim.x, red, cfin);
         else
-            cr_reduce<NM>(a.cpart[2], (int)gridDim.x, red, cfin);
+            cr_reduce<NM, kBlock3>(a.cpart[2], (int)gridDim.x, red, cfin);
         if (tid < NM) tot[0][tid] = x0;
         if (STAGE == 4 && tid < 2 * NM) tot[1 + tid / NM][tid % NM] = x1;
         if (tid < (STAGE == 3 ? 2 * NM : NM)) {
@@ -225,7 +235,7 @@ __global__ void __launch_bounds__(kBlock, OSC3_MIN_BLOCKS) k_stage3(StepArgs a) 
                           ctl2 ? CS.A[2] : (STAGE ? ctl->A[2] : 0.0)};
     const int tr0 = c1 > c0 ? (int)div_e(c0, a.e_magic, a.e_shift) : 0;
     const int ntr = c1 > c0 ? (int)div_e(c1 - 1, a.e_magic, a.e_shift) - tr0 + 1 : 0;
-    for (int i = tid; i < ntr; i += kBlock) {
+    for (int i = tid; i < ntr; i += kBlock3) {
         const int traj = tr0 + i;
         const int th = a.t_lo + traj / a.P;
         Geo G[3];
@@ -282,25 +292,25 @@ __global__ void __launch_bounds__(kBlock, OSC3_MIN_BLOCKS) k_stage3(StepArgs a) 
             for (int j = 0; j < PF; ++j) {
                 if (j >= 18 && !stash) break;
                 const double* sp = (j < 18 ? src0 : a.stash) + (size_t)((2 * ((j % 18) / 6) + pc) * 6 + j % 6) * np;
-                cp_async8_ca(pf + ((size_t)buf * PF + j) * kBlock + tid, sp + cl);
+                cp_async8_ca(pf + ((size_t)buf * PF + j) * kBlock3 + tid, sp + cl);
             }
         }
         cp_async_commit();
     };
     issue(c0 + tid, 0);
     int it = 0;
-    for (int cell = c0 + tid; cell < c1; cell += kBlock, ++it) {
+    for (int cell = c0 + tid; cell < c1; cell += kBlock3, ++it) {
         const int traj = (int)div_e(cell, a.e_magic, a.e_shift);
         const int e = cell - traj * a.E;
         const TrajRec3& R = rec[traj - tr0];
         cp_async_wait_all();  // this thread's copies of this cell
-        issue(cell + kBlock, (it + 1) & 1);
-        const double* cur_pf = pf + (size_t)(it & 1) * PF * kBlock + tid;
+        issue(cell + kBlock3, (it + 1) & 1);
+        const double* cur_pf = pf + (size_t)(it & 1) * PF * kBlock3 + tid;
         double x[3][6];
 #pragma unroll
         for (int f = 0; f < 3; ++f)
 #pragma unroll
-            for (int c = 0; c < 6; ++c) x[f][c] = cur_pf[(size_t)(f * 6 + c) * kBlock];
+            for (int c = 0; c < 6; ++c) x[f][c] = cur_pf[(size_t)(f * 6 + c) * kBlock3];
         double g[3];
 #pragma unroll
         for (int f = 0; f < 3; ++f) g[f] = __ldg(a.g + (size_t)(2 * f + pc) * a.E + e);
@@ -390,7 +400,7 @@ __global__ void __launch_bounds__(kBlock, OSC3_MIN_BLOCKS) k_stage3(StepArgs a) 
 #pragma unroll
                     for (int f = 0; f < 3; ++f)
 #pragma unroll
-                        for (int c = 0; c < 6; ++c) h2[f][c] = cur_pf[(size_t)(18 + f * 6 + c) * kBlock];
+                        for (int c = 0; c < 6; ++c) h2[f][c] = cur_pf[(size_t)(18 + f * 6 + c) * kBlock3];
                 } else {
                     const Mat3 um = prop(0, 0), uh = prop(2, 1);
 #pragma unroll
@@ -451,7 +461,7 @@ __global__ void __launch_bounds__(kBlock, OSC3_MIN_BLOCKS) k_stage3(StepArgs a) 
     // now; sized for NV + 1 columns), stored [value][block] (a reducer's
     // loads of one value across blocks coalesce)
     const bool cr_out = a.cr3 && (STAGE == 2 || STAGE == 3 || STAGE == 4);  // reduced by every block of S3 / S4 / next S2
-    block_cols_store<NV>(acc, emax, pf, (cr_out ? a.cpart[Tr::slot] : a.partials) + blockIdx.x, gridDim.x);
+    block_cols_store<NV, kBlock3>(acc, emax, pf, (cr_out ? a.cpart[Tr::slot] : a.partials) + blockIdx.x, gridDim.x);
     if (cr_out) return;
     if (tid == 0) {
         __threadfence();
@@ -463,7 +473,7 @@ __global__ void __launch_bounds__(kBlock, OSC3_MIN_BLOCKS) k_stage3(StepArgs a) 
     __threadfence();
     __shared__ double fin[2 * kNM3Max + 1];
     __shared__ double pub[kSlotDoubles];
-    cols_reduce<NV>(a.partials, (int)gridDim.x, fin);
+    cols_reduce<NV, kBlock3>(a.partials, (int)gridDim.x, fin);
     if (tid < kSlotDoubles) {
         // slot layout: per set 36 doubles (9 x up to 4 geometric moments),
         // S2 = sums1 | sums2, S4 error at index 36
@@ -500,12 +510,12 @@ __global__ void __launch_bounds__(kBlock, OSC3_MIN_BLOCKS) k_stage3(StepArgs a) 
 inline size_t stage3_smem_bytes(int ntr_max, int stage) {
     // (the columns double as the block-partial scratch: 2 x 18 moments + max in S2)
     const int cols = std::max(2 * stage3_pf_planes(stage), 2 * kNM3Max + 1);
-    return stage3_rec_bytes(ntr_max) + (size_t)cols * kBlock * sizeof(double);
+    return stage3_rec_bytes(ntr_max) + (size_t)cols * kBlock3 * sizeof(double);
 }
 
 // Single GPU: the control update of a batch's last step (one block).
 template <int MODEL>
-__global__ void __launch_bounds__(kBlock, 1) k_finalize3(StepArgs a) {
+__global__ void __launch_bounds__(kBlock3, 1) k_finalize3(StepArgs a) {
     __shared__ StageShared S;
     grid_dependency_wait();
     cr_control3<MODEL == 0 ? 9 : 18>(a, S, true, nullptr);

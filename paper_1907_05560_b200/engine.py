@@ -413,6 +413,22 @@ def debug_evolve_bin(h, dl, psi, path: int = 0, device: int = 0):
     return out
 
 
+def debug_exp3(H9, tau, path: int = 0, device: int = 0):
+    """exp(-i H tau) of packed 3x3 Hermitian matrices through the device code
+    of the 3-flavour stages (csrc/su3_exp.cuh).  H9 [n,9], tau [n] -> complex
+    [n,3,3]."""
+    import numpy as np
+
+    H9 = np.ascontiguousarray(H9, dtype=np.float64).reshape(-1, 9)
+    n = H9.shape[0]
+    tau = np.ascontiguousarray(tau, dtype=np.float64).reshape(n)
+    out = np.zeros((n, 18))
+    dp = C.POINTER(C.c_double)
+    check(lib().osc_debug_exp3(device, n, H9.ctypes.data_as(dp), tau.ctypes.data_as(dp),
+                               out.ctypes.data_as(dp), path))
+    return (out[:, 0::2] + 1j * out[:, 1::2]).reshape(n, 3, 3)
+
+
 def comm_unique_id() -> bytes:
     buf = C.create_string_buffer(128)
     check(lib().osc_comm_unique_id(buf))

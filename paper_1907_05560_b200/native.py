@@ -89,7 +89,7 @@ SYMBOLS = [
     "osc_set_state_device", "osc_get_state_device", "osc_trial_step_error", "osc_run", "osc_run_dumps", "osc_extract_mode2",
     "osc_max_norm_dev", "osc_begin", "osc_enqueue_steps", "osc_query", "osc_synchronize",
     "osc_stream", "osc_launches_per_step", "osc_debug_sums", "osc_set_schedule", "osc_set_launch_mode", "osc_get_launch_mode", "osc_comm_export", "osc_comm_connect", "osc_launch_count",
-    "osc_fp64_peak", "osc_profile_stages", "osc_debug_evolve_bin", "osc_debug_trace", "osc_env_build", "osc_env_desc", "osc_env_destroy", "osc_fermi_integral",
+    "osc_fp64_peak", "osc_profile_stages", "osc_debug_evolve_bin", "osc_debug_exp3", "osc_debug_trace", "osc_env_build", "osc_env_desc", "osc_env_destroy", "osc_fermi_integral",
     "osc_create_group", "osc_group_info", "osc_device_count",
 ]
 
@@ -144,6 +144,7 @@ def lib() -> C.CDLL:
     L.osc_profile_stages.argtypes = [vp, C.c_int, C.POINTER(C.c_float)]
     L.osc_debug_trace.argtypes = [C.POINTER(C.c_ulonglong), C.c_size_t]
     L.osc_debug_evolve_bin.argtypes = [C.c_int, C.c_size_t, _dp, _dp, _dp, _dp, C.c_int]
+    L.osc_debug_exp3.argtypes = [C.c_int, C.c_size_t, _dp, _dp, _dp, C.c_int]
     L.osc_env_build.argtypes = [C.POINTER(OscParams), C.POINTER(vp)]
     L.osc_env_desc.argtypes = [vp, C.POINTER(OscDesc), _dp]
     L.osc_env_destroy.argtypes = [vp]
