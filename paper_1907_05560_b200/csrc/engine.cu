@@ -237,7 +237,7 @@ struct OscCtx {
 
     DevBuf<double> cos2, sin0, cphi, sphi, vac11, vac12, g, ktab_g;
     DevBuf<double> cpart[4];  // single GPU: block partials of S2, S3, S4 (consumer-side reduction)
-    DevBuf<double> psi[2], bloch[2], stash, xbuf, xsend, partials, staging;
+    DevBuf<double> psi[2], bloch[2], stash, ustash, xbuf, xsend, partials, staging;
     // snapshot I/O: spectrum weights [nsp][E] (mode 2), mode-2 output, the
     // second packing buffer and pinned host buffers of the async dumps
     DevBuf<double> fw, mode2buf, staging2;
@@ -855,6 +855,7 @@ int osc_create(const OscDesc* desc, const OscComm* comm, OscCtx** out) {
         a.e_shift = c->e_shift;
         a.schedule = c->schedule;
         c->stash.alloc((size_t)c->npad * (c->nflav == 3 ? kSt3Planes : c->nplanes));
+        if (c->nflav == 2) c->ustash.alloc((size_t)c->npad * kUPlanes);
         a.Rnu = desc->Rnu;
         a.dcos2 = 1.0 / c->T;
         a.phi_measure = desc->model >= OSC_MODEL_EXT_BULB ? 1.0 / c->P : 1.0;
@@ -885,6 +886,7 @@ int osc_create(const OscDesc* desc, const OscComm* comm, OscCtx** out) {
         a.bloch_buf[0] = c->bloch[0].p;
         a.bloch_buf[1] = c->bloch[1].p;
         a.stash = c->stash.p;
+        a.ustash = c->ustash.p;
         a.xbuf = c->xbuf.p;
         a.xsend = c->coll ? c->xsend.p : c->xbuf.p;
         a.p2p = 0;
