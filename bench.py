@@ -373,7 +373,9 @@ def main():
         # psi0 + write psi_new, 256 B per beam-step) all moves in S4; the
         # schedule adds its own intermediates (Bloch planes 48 B, P stash 64 B)
         alg_bytes = {"S2": 0, "S3": 0, "S4": 256}[names[k]]
-        sched_bytes = {"S2": 48, "S3": 48 + 64, "S4": 128 + 64 + 128 + 48}[names[k]]
+        # (S2 -> S3 scalars: 32 B written by S2, read by S3; they and the P stash
+        # stay in L2 and are dropped there after their one read)
+        sched_bytes = {"S2": 48 + 32, "S3": 48 + 32 + 64, "S4": 128 + 64 + 128 + 48}[names[k]]
         hbm_ach = alg_bytes * cells_total / (stage_ms[k] * 1e-3) / 1e9
         hbm_frac = hbm_ach / hbm_peak[0]
         fp64_view = {"achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
@@ -389,6 +391,7 @@ def main():
                 "unit": "GB/s" if hbm_bound else "TFLOP/s",
                 "frac": hbm_frac if hbm_bound else achieved / peak,
                 "traffic": traffic,
+                "traffic_warm": W.get("traffic_warm", {}).get(names[k]),
                 "algorithmic_bytes_per_cell": alg_bytes,
                 "peak_source": hbm_peak[1] if hbm_bound else fp64_view["peak_source"],
                 "stage_ms": dict(zip(names, stage_ms)),
@@ -398,8 +401,9 @@ def main():
                                         "note": "all bytes this schedule moves in the kernel (state, "
                                                 "propagator stash, Bloch planes)"},
                 "fp64_view": fp64_view,
-                "traffic_note": "ncu dram__bytes_read+write per launch (profiles/fp64_work.json, "
-                                "cold-cache ncu replay; writes still in L2 at kernel end not counted)",
+                "traffic_note": "ncu dram__bytes_read+write per launch (profiles/fp64_work.json): traffic from the "
+                                "--set full capture (cold-cache replay; writes still in L2 at kernel end not "
+                                "counted), traffic_warm with --cache-control none in the running pipeline",
                 "step": {"W_per_cell": w_step, "achieved": step_achieved,
                          "frac_fp64": step_achieved / peak,
                          "hbm_compulsory_gbs": 256 * cells_total / (ms / a.steps * 1e-3) / 1e9,
