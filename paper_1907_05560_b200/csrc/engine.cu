@@ -798,7 +798,7 @@ int osc_create(const OscDesc* desc, const OscComm* comm, OscCtx** out) {
             c->rch = (c->ncell + c->nsm - 1) / c->nsm;
             c->rntr = c->rch / c->E + 2;
             c->rsmem = resident_smem_bytes(c->rch, c->rntr, c->E);
-            if (c->rsmem <= 200 * 1024 && OSC_DEBUG_MODE == 0) {
+            if (c->rsmem <= 200 * 1024) {
                 const ResidentFn rf = resident_kernel(desc->model);
                 set_max_dynamic_smem(rf, c->device);
                 int rper = 0;
