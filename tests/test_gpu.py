@@ -238,6 +238,34 @@ def test_full_size_configs2_properties():
     assert np.max(np.abs(t - 1.0)) <= TRACE_TOL
 
 
+@pytest.mark.gpu
+def test_s2_to_s3_scalars_fallback_cells_match_the_recompute_path():
+    """S2 hands Um's scalars to S3 through L2; cells where S2's fast path does
+    not apply (|lambda dl| > 1e9, or lambda dl < 1e-12 where s = dl) are
+    marked and S3 recomputes them exactly as without the hand-over.  A trial
+    step with an enormous or a vanishing dr puts every cell on those paths;
+    the embedded error (a function of S3's propagator P through S4) must then
+    carry the bits of the schedule whose S4 recomputes P from scratch, in the
+    stage kernels and (to rounding) in the resident kernel, which never uses
+    the hand-over.  beam.hpp:105-121 (evolve_bin's branches)."""
+    cfg = baseline_config("configs0", Abins=24, Ebins=40, R0=50, Rn=60, dr=1e-3, max_dr=1e-3, Ts=4)
+    env, eng = make(cfg)
+    eng.set_launch_mode(Engine.LAUNCH_STAGES)
+    for dr in (3e13, 1e-21, 1e-3):
+        errs = []
+        for sched in (0, 1):
+            eng.set_schedule(sched)
+            errs.append(eng.trial_step_error(50.0, dr))
+        assert math.isfinite(errs[0]) and errs[0] >= 0.0, (dr, errs)
+        assert errs[0] == errs[1], (dr, errs)
+    # the ordinary step size also agrees with the resident kernel's own propagators
+    eng.set_schedule(1)
+    e_stage = eng.trial_step_error(50.0, 1e-3)
+    eng.set_launch_mode(Engine.LAUNCH_RESIDENT)
+    e_res = eng.trial_step_error(50.0, 1e-3)
+    assert abs(e_stage - e_res) <= 1e-12 * max(1.0, abs(e_stage))
+
+
 # ---------------------------------------------------- test_solver.cpp restated
 def base_config():
     return parse_config(
