@@ -388,7 +388,7 @@ __global__ void __launch_bounds__(kBlock, 1)
 #pragma unroll
                     for (int c = 0; c < 4; ++c) {
                         xr[(size_t)(s * 4 + c) * ch + k] = out[c];
-                        emax = fmax(emax, fabs(d[c]));
+                        emax = max_abs(emax, d[c]);
                     }
                     bloch_add(out, K, s, B);
                 }

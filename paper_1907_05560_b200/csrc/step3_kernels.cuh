@@ -451,7 +451,7 @@ __global__ void __launch_bounds__(kBlock3, OSC3_MIN_BLOCKS) k_stage3(StepArgs a)
                 double av[6];
                 apply3(Q, x[f], av);
 #pragma unroll
-                for (int c = 0; c < 6; ++c) emax = fmax(emax, fabs(av[c] - out[f][c]));
+                for (int c = 0; c < 6; ++c) emax = max_abs(emax, av[c] - out[f][c]);
             }
         }
     }
