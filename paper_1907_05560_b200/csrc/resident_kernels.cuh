@@ -148,7 +148,7 @@ __global__ void __launch_bounds__(kBlock, 1)
         const double* g = a.psi0_buf[S.c.cur];
         for (int i = tid; i < kPlanes * n; i += kBlock) {
             const int p = i / n, k = i - p * n;
-            buf[0][(size_t)p * ch + k] = __ldcg(g + (size_t)p * np + c0 + k);
+            buf[0][(size_t)p * ch + k] = __ldcg(g + psi_off(a, p, (size_t)c0 + k));
         }
         for (int i = tid; i < 6 * a.E; i += kBlock) {
             const int row = i / a.E, e = i - row * a.E;
@@ -419,7 +419,7 @@ __global__ void __launch_bounds__(kBlock, 1)
         double* g = a.psi0_buf[S.c.cur];
         for (int i = tid; i < kPlanes * n; i += kBlock) {
             const int p = i / n, k = i - p * n;
-            g[(size_t)p * np + c0 + k] = buf[lb][(size_t)p * ch + k];
+            g[psi_off(a, p, (size_t)c0 + k)] = buf[lb][(size_t)p * ch + k];
         }
     }
     if (blockIdx.x == 0) {
