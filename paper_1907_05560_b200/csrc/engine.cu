@@ -661,9 +661,11 @@ int osc_create(const OscDesc* desc, const OscComm* comm, OscCtx** out) {
         upload(c->g, g.data(), g.size());
         if (c->nflav == 2) {  // contiguous per-energy table for the stage kernels' bulk copy
             std::vector<double> kt((size_t)((6 * c->E + 1) & ~1), 0.0);
-            std::copy(desc->vac_h11, desc->vac_h11 + c->E, kt.begin());
-            std::copy(desc->vac_h12, desc->vac_h12 + c->E, kt.begin() + c->E);
-            std::copy(g.begin(), g.end(), kt.begin() + 2 * (size_t)c->E);
+            for (int e = 0; e < c->E; ++e) {  // [E][6]: v11, v12, g0..g3 (three 16-byte loads per cell)
+                kt[6 * (size_t)e] = desc->vac_h11[e];
+                kt[6 * (size_t)e + 1] = desc->vac_h12[e];
+                for (int s = 0; s < 4; ++s) kt[6 * (size_t)e + 2 + s] = g[(size_t)s * c->E + e];
+            }
             upload(c->ktab_g, kt.data(), kt.size());
         }
         upload(c->fw, fw, (size_t)nsp * c->E);
