@@ -303,7 +303,7 @@ struct OscCtx {
         cudaLaunchConfig_t cfg{};
         cfg.gridDim = dim3((nflav == 2 && (stage == 2 || stage == 3)) ? nblocks23 : nblocks);
         cfg.blockDim = dim3(nflav == 3 ? kBlock3 : kBlock);
-        cfg.dynamicSmemBytes = nflav == 3 ? stage3_smem_bytes(ntr_max, stage) : stage_smem_bytes(stage, schedule, ntr_max, E, rec_stride);
+        cfg.dynamicSmemBytes = nflav == 3 ? stage3_smem_bytes(ntr_max, stage, args.uf_cols) : stage_smem_bytes(stage, schedule, ntr_max, E, rec_stride);
         cfg.stream = stream;
         cudaLaunchAttribute attr[1];
         attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -856,6 +856,8 @@ int osc_create(const OscDesc* desc, const OscComm* comm, OscCtx** out) {
         a.e_magic = c->e_magic;
         a.e_shift = c->e_shift;
         a.schedule = c->schedule;
+        // 3 flavours: S4's U1 columns where the block's shared memory still holds them
+        a.uf_cols = c->nflav == 3 && stage3_smem_bytes(c->ntr_max, 4, 1) <= 200 * 1024;
         c->stash.alloc((size_t)c->npad * (c->nflav == 3 ? kSt3Planes : c->nplanes));
         if (c->nflav == 2) c->ustash.alloc((size_t)c->npad * kUPlanes);
         a.Rnu = desc->Rnu;

@@ -285,6 +285,7 @@ __global__ void __launch_bounds__(kBlock3, OSC3_MIN_BLOCKS) k_stage3(StepArgs a)
     // = Um psi0 from S2), [18, 36) (S4 with the stash): half2 from S3.
     constexpr int PF = stage3_pf_planes(STAGE);
     double* pf = reinterpret_cast<double*>(dsm3 + stage3_rec_bytes(a.ntr_max));
+    double* ufc = pf + (size_t)2 * PF * kBlock3;  // S4, a.uf_cols: [18][kBlock3]
     const double* src0 = (STAGE == 3 && stash) ? a.stash : psi0;
     auto issue = [&](int cl, int buf) {
         if (cl < c1) {
@@ -305,6 +306,16 @@ __global__ void __launch_bounds__(kBlock3, OSC3_MIN_BLOCKS) k_stage3(StepArgs a)
         const TrajRec3& R = rec[traj - tr0];
         cp_async_wait_all();  // this thread's copies of this cell
         issue(cell + kBlock3, (it + 1) & 1);
+        if (STAGE == 4 && stash && a.uf_cols) {
+            // U1 (full1's propagator, stashed by S2) is needed at the end of
+            // the cell: copied into this thread's column now, so its L2
+            // latency hides behind the exponentials (read straight from
+            // global it stalled S4 ~20 % of the time)
+#pragma unroll
+            for (int j = 0; j < 18; ++j)
+                cp_async8_ca(ufc + (size_t)j * kBlock3 + tid, a.stash + (size_t)(kSt3Uf + pc * 18 + j) * np + cell);
+            cp_async_commit();
+        }
         const double* cur_pf = pf + (size_t)(it & 1) * PF * kBlock3 + tid;
         double x[3][6];
 #pragma unroll
@@ -431,7 +442,14 @@ __global__ void __launch_bounds__(kBlock3, OSC3_MIN_BLOCKS) k_stage3(StepArgs a)
             // from S2 (stash) or is recomputed
             const Mat3 u2 = prop(1, 2);
             Mat3 Q;
-            if (stash) {
+            if (stash && a.uf_cols) {
+                cp_async_wait_all();  // (the column copy above; the next cell's operands have landed long since)
+#pragma unroll
+                for (int i = 0; i < 3; ++i)
+#pragma unroll
+                    for (int j = 0; j < 3; ++j)
+                        Q.m[i][j] = Cx{ufc[(size_t)((i * 3 + j) * 2) * kBlock3 + tid], ufc[(size_t)((i * 3 + j) * 2 + 1) * kBlock3 + tid]};
+            } else if (stash) {
 #pragma unroll
                 for (int i = 0; i < 3; ++i)
 #pragma unroll
@@ -507,9 +525,10 @@ __global__ void __launch_bounds__(kBlock3, OSC3_MIN_BLOCKS) k_stage3(StepArgs a)
 
 // Dynamic shared memory of a 3-flavour stage: trajectory records, then the
 // double-buffered per-thread prefetch columns.
-inline size_t stage3_smem_bytes(int ntr_max, int stage) {
-    // (the columns double as the block-partial scratch: 2 x 18 moments + max in S2)
-    const int cols = std::max(2 * stage3_pf_planes(stage), 2 * kNM3Max + 1);
+inline size_t stage3_smem_bytes(int ntr_max, int stage, int uf_cols = 0) {
+    // (the columns double as the block-partial scratch: 2 x 18 moments + max in S2;
+    // S4 with uf_cols: 18 more single-buffered columns for U1)
+    const int cols = std::max(2 * stage3_pf_planes(stage) + ((stage == 4 && uf_cols) ? 18 : 0), 2 * kNM3Max + 1);
     return stage3_rec_bytes(ntr_max) + (size_t)cols * kBlock3 * sizeof(double);
 }
 
