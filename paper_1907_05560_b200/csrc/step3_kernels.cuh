@@ -148,8 +148,16 @@ __device__ __forceinline__ void cr_control3(const StepArgs& a, StageShared& S, b
 #endif
 __host__ __device__ constexpr int stage3_pf_planes(int stage) { return stage == 4 ? 36 : 18; }
 __host__ __device__ constexpr size_t stage3_rec_bytes(int ntr_max) { return ((size_t)ntr_max * sizeof(TrajRec3) + 15) & ~(size_t)15; }
-__device__ __forceinline__ void cp_async8_ca(void* dst, const void* src) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+__device__ __forceinline__ void cp_async16_cg(void* dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+// Pair plane q (the (re, im) pair of one amplitude or matrix entry) of a cell
+// in a buffer of planes of pairs.
+__device__ __forceinline__ double2* pair_at(double* base, int q, size_t np, size_t cell) {
+    return reinterpret_cast<double2*>(base + 2 * ((size_t)q * np + cell));
+}
+__device__ __forceinline__ const double2* pair_at(const double* base, int q, size_t np, size_t cell) {
+    return reinterpret_cast<const double2*>(base + 2 * ((size_t)q * np + cell));
 }
 __device__ __noinline__ Mat3 exp_herm3_ool(const Herm3& H, double tau) { return exp_herm3(H, tau); }
 
@@ -285,15 +293,16 @@ __global__ void __launch_bounds__(kBlock3, OSC3_MIN_BLOCKS) k_stage3(StepArgs a)
     // = Um psi0 from S2), [18, 36) (S4 with the stash): half2 from S3.
     constexpr int PF = stage3_pf_planes(STAGE);
     double* pf = reinterpret_cast<double*>(dsm3 + stage3_rec_bytes(a.ntr_max));
-    double* ufc = pf + (size_t)2 * PF * kBlock3;  // S4, a.uf_cols: [18][kBlock3]
+    double2* pf2 = reinterpret_cast<double2*>(pf);           // the same columns as (re, im) pairs: [2][PF / 2][kBlock3]
+    double2* ufc = pf2 + (size_t)PF * kBlock3;               // S4, a.uf_cols: [9][kBlock3]
     const double* src0 = (STAGE == 3 && stash) ? a.stash : psi0;
     auto issue = [&](int cl, int buf) {
         if (cl < c1) {
 #pragma unroll
-            for (int j = 0; j < PF; ++j) {
-                if (j >= 18 && !stash) break;
-                const double* sp = (j < 18 ? src0 : a.stash) + (size_t)((2 * ((j % 18) / 6) + pc) * 6 + j % 6) * np;
-                cp_async8_ca(pf + ((size_t)buf * PF + j) * kBlock3 + tid, sp + cl);
+            for (int j = 0; j < PF / 2; ++j) {  // pair j % 9 = 3 f + amplitude of species 2 f + pc
+                if (j >= 9 && !stash) break;
+                cp_async16_cg(pf2 + ((size_t)buf * (PF / 2) + j) * kBlock3 + tid,
+                              pair_at(j < 9 ? src0 : a.stash, (2 * ((j % 9) / 3) + pc) * 3 + j % 3, np, cl));
             }
         }
         cp_async_commit();
@@ -312,16 +321,18 @@ __global__ void __launch_bounds__(kBlock3, OSC3_MIN_BLOCKS) k_stage3(StepArgs a)
             // latency hides behind the exponentials (read straight from
             // global it stalled S4 ~20 % of the time)
 #pragma unroll
-            for (int j = 0; j < 18; ++j)
-                cp_async8_ca(ufc + (size_t)j * kBlock3 + tid, a.stash + (size_t)(kSt3Uf + pc * 18 + j) * np + cell);
+            for (int j = 0; j < 9; ++j)
+                cp_async16_cg(ufc + (size_t)j * kBlock3 + tid, pair_at(a.stash, kSt3Uf / 2 + pc * 9 + j, np, cell));
             cp_async_commit();
         }
-        const double* cur_pf = pf + (size_t)(it & 1) * PF * kBlock3 + tid;
+        const double2* cur_pf = pf2 + (size_t)(it & 1) * (PF / 2) * kBlock3 + tid;
         double x[3][6];
 #pragma unroll
-        for (int f = 0; f < 3; ++f)
-#pragma unroll
-            for (int c = 0; c < 6; ++c) x[f][c] = cur_pf[(size_t)(f * 6 + c) * kBlock3];
+        for (int j = 0; j < 9; ++j) {
+            const double2 v = cur_pf[(size_t)j * kBlock3];
+            x[j / 3][2 * (j % 3)] = v.x;
+            x[j / 3][2 * (j % 3) + 1] = v.y;
+        }
         double g[3];
 #pragma unroll
         for (int f = 0; f < 3; ++f) g[f] = __ldg(a.g + (size_t)(2 * f + pc) * a.E + e);
@@ -360,14 +371,14 @@ __global__ void __launch_bounds__(kBlock3, OSC3_MIN_BLOCKS) k_stage3(StepArgs a)
 #pragma unroll
                 for (int f = 0; f < 3; ++f)
 #pragma unroll
-                    for (int c = 0; c < 6; ++c) __stcg(a.stash + (size_t)((2 * f + pc) * 6 + c) * np + cell, y[f][c]);
+                    for (int h = 0; h < 3; ++h)
+                        __stcg(pair_at(a.stash, (2 * f + pc) * 3 + h, np, cell), make_double2(y[f][2 * h], y[f][2 * h + 1]));
 #pragma unroll
                 for (int i = 0; i < 3; ++i)
 #pragma unroll
-                    for (int j = 0; j < 3; ++j) {
-                        __stcg(a.stash + (size_t)(kSt3Uf + pc * 18 + (i * 3 + j) * 2) * np + cell, uf.m[i][j].re);
-                        __stcg(a.stash + (size_t)(kSt3Uf + pc * 18 + (i * 3 + j) * 2 + 1) * np + cell, uf.m[i][j].im);
-                    }
+                    for (int j = 0; j < 3; ++j)
+                        __stcg(pair_at(a.stash, kSt3Uf / 2 + pc * 9 + i * 3 + j, np, cell),
+                               make_double2(uf.m[i][j].re, uf.m[i][j].im));
             }
 #pragma unroll
             for (int f = 0; f < 3; ++f) apply3(uf, x[f], y[f]);
@@ -393,7 +404,8 @@ __global__ void __launch_bounds__(kBlock3, OSC3_MIN_BLOCKS) k_stage3(StepArgs a)
                 apply3(uh, mid, hh[f]);
                 if (stash)
 #pragma unroll
-                    for (int c = 0; c < 6; ++c) __stcg(a.stash + (size_t)((2 * f + pc) * 6 + c) * np + cell, hh[f][c]);
+                    for (int h = 0; h < 3; ++h)
+                        __stcg(pair_at(a.stash, (2 * f + pc) * 3 + h, np, cell), make_double2(hh[f][2 * h], hh[f][2 * h + 1]));
             }
             weighted_rho3(hh, g, pc, Rr);
 #pragma unroll
@@ -409,9 +421,11 @@ __global__ void __launch_bounds__(kBlock3, OSC3_MIN_BLOCKS) k_stage3(StepArgs a)
                 double h2[3][6];
                 if (stash) {  // (prefetched)
 #pragma unroll
-                    for (int f = 0; f < 3; ++f)
-#pragma unroll
-                        for (int c = 0; c < 6; ++c) h2[f][c] = cur_pf[(size_t)(18 + f * 6 + c) * kBlock3];
+                    for (int j = 0; j < 9; ++j) {
+                        const double2 v = cur_pf[(size_t)(9 + j) * kBlock3];
+                        h2[j / 3][2 * (j % 3)] = v.x;
+                        h2[j / 3][2 * (j % 3) + 1] = v.y;
+                    }
                 } else {
                     const Mat3 um = prop(0, 0), uh = prop(2, 1);
 #pragma unroll
@@ -426,10 +440,10 @@ __global__ void __launch_bounds__(kBlock3, OSC3_MIN_BLOCKS) k_stage3(StepArgs a)
                     double f3[6];
                     apply3(u3, x[f], f3);
 #pragma unroll
-                    for (int c = 0; c < 6; ++c) {
-                        out[f][c] = (h2[f][c] + f3[c]) * 0.5;  // evolve_avg, beam.cpp:188-218
-                        res[(size_t)((2 * f + pc) * 6 + c) * np + cell] = out[f][c];
-                    }
+                    for (int c = 0; c < 6; ++c) out[f][c] = (h2[f][c] + f3[c]) * 0.5;  // evolve_avg, beam.cpp:188-218
+#pragma unroll
+                    for (int h = 0; h < 3; ++h)
+                        *pair_at(res, (2 * f + pc) * 3 + h, np, cell) = make_double2(out[f][2 * h], out[f][2 * h + 1]);
                 }
             }
             weighted_rho3(out, g, pc, Rr);
@@ -448,14 +462,19 @@ __global__ void __launch_bounds__(kBlock3, OSC3_MIN_BLOCKS) k_stage3(StepArgs a)
                 for (int i = 0; i < 3; ++i)
 #pragma unroll
                     for (int j = 0; j < 3; ++j)
-                        Q.m[i][j] = Cx{ufc[(size_t)((i * 3 + j) * 2) * kBlock3 + tid], ufc[(size_t)((i * 3 + j) * 2 + 1) * kBlock3 + tid]};
+                    {
+                        const double2 v = ufc[(size_t)(i * 3 + j) * kBlock3 + tid];
+                        Q.m[i][j] = Cx{v.x, v.y};
+                    }
             } else if (stash) {
 #pragma unroll
                 for (int i = 0; i < 3; ++i)
 #pragma unroll
                     for (int j = 0; j < 3; ++j)
-                        Q.m[i][j] = Cx{__ldcg(a.stash + (size_t)(kSt3Uf + pc * 18 + (i * 3 + j) * 2) * np + cell),
-                                       __ldcg(a.stash + (size_t)(kSt3Uf + pc * 18 + (i * 3 + j) * 2 + 1) * np + cell)};
+                    {
+                        const double2 v = __ldcg(pair_at(a.stash, kSt3Uf / 2 + pc * 9 + i * 3 + j, np, cell));
+                        Q.m[i][j] = Cx{v.x, v.y};
+                    }
             } else {
                 Q = prop(0, 2);
             }
@@ -568,7 +587,7 @@ __global__ void k_init3(StepArgs a, double eps) {
             c[2 * o2] = u2;
             c[2 * o2 + 1] = v2;
         }
-        for (int k = 0; k < 6; ++k) psi[(size_t)(s * 6 + k) * np + cell] = c[k];
+        for (int k = 0; k < 6; ++k) psi[psi_off(a, s * 6 + k, cell)] = c[k];
     }
 }
 
