@@ -3,7 +3,7 @@
 # step, the configs[0] resident kernel and the configs[1] 3-flavour stages.
 # Summaries go to profiles/ by hand (tools/ncu_summary.py, tools/ncu_stalls.py,
 # tools/ncu_mix.py).  usage: bash tools/measure_round.sh [tag]
-TAG=${1:-r11}
+TAG=${1:-r12}
 timeout 1500 python -m pytest tests -m gpu -q --timeout=600 > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?"; tail -2 gpurun_out/pytest_gpu.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?"
 timeout 900 python bench.py > gpurun_out/bench.log 2>&1; echo "bench rc=$?"
