@@ -203,16 +203,14 @@ __global__ void __launch_bounds__(kBlock, 1)
         }
     }
 
-    for (int step = 0; started && step < nsteps; ++step) {
-        if (S.c.terminate | S.c.status | S.c.pause) break;
-        const double r = S.c.r, dr = S.c.dr;
+    // The geometric part of a step's trajectory records (dl slots, direction
+    // factors, fold coefficients at r+dr (fold[0]) and r+dr/2 (fold[1]);
+    // geometry.cpp:66-216): a function of (r, dr) only, so the next step's is
+    // built while S4's all-reduce completes, for the outcome "accepted, next
+    // step at the capped size", and kept if the control then decides exactly
+    // that (every fixed-step run; same operations, same bits).
+    auto geometry = [&](double r, double dr) {
         const double rk[3] = {r, r + 0.5 * dr, r + dr};
-        const double Am[3] = {S.c.A[0], S.c.A[1], S.c.A[2]};
-        const double* x0 = buf[lb];
-        double* xr = buf[lb ^ 1];
-
-        // trajectory records of the step: dl slots, fold coefficients at
-        // r+dr (fold[0]) and r+dr/2 (fold[1]), H0 (geometry.cpp:66-216)
         for (int i = tid; i < ntr; i += kBlock) {
             const int traj = tr0 + i;
             const int th = a.t_lo + traj / a.P, ph = traj % a.P;
@@ -232,6 +230,24 @@ __global__ void __launch_bounds__(kBlock, 1)
                 R.fold[0][j] = G[2].f[j];
                 R.fold[1][j] = G[1].f[j];
             }
+        }
+    };
+    double r_sp = 0.0, dr_sp = 0.0;  // the (r, dr) the records' geometry was built for ahead of time
+    bool have_sp = false;
+
+    for (int step = 0; started && step < nsteps; ++step) {
+        if (S.c.terminate | S.c.status | S.c.pause) break;
+        const double r = S.c.r, dr = S.c.dr;
+        const double rk[3] = {r, r + 0.5 * dr, r + dr};
+        const double Am[3] = {S.c.A[0], S.c.A[1], S.c.A[2]};
+        const double* x0 = buf[lb];
+        double* xr = buf[lb ^ 1];
+
+        // trajectory records of the step: the geometry (unless built ahead),
+        // then H0 from the moments of psi0
+        if (!(have_sp && r == r_sp && dr == dr_sp)) geometry(r, dr);
+        for (int i = tid; i < ntr; i += kBlock) {  // (each thread reads the direction factors it wrote)
+            TrajRec& R = rec[i];
             double hv[3];
             assemble<MODEL>(S.tot0, rk[0], a.Rnu, R.n[0], hv);
             R.hb[0][0] = hv[0] + 0.5 * Am[0];
@@ -395,7 +411,17 @@ __global__ void __launch_bounds__(kBlock, 1)
                 bloch_sum(B, Rr);
                 fold_acc<NM>(acc, Rr, R->fold[0]);
             }
-            if (!res_allreduce<NM>(acc, emax, part, bar, phase, S, S.fin, scratch)) break;
+            res_arrive<NM>(acc, emax, part, bar, phase, S, scratch);
+            // while the other blocks arrive: the next step's geometry (the
+            // records are free: every thread has passed the barrier in
+            // res_arrive), predicted as ctl_advance computes it for an
+            // accepted step whose next size hits dr_max
+            r_sp = r + dr;
+            dr_sp = S.c.dr_max;
+            if (r_sp + dr_sp > S.c.Rn) dr_sp = S.c.Rn - r_sp;
+            geometry(r_sp, dr_sp);
+            have_sp = true;
+            if (!res_finish<NM>(part, bar, phase, S, S.fin)) break;
             if (tid <= NM) S.totn[tid] = S.fin[tid];
         }
 
