@@ -146,6 +146,26 @@ def test_configs2_full_size_vs_compiled_reference(ref):
     assert np.max(np.abs(tg - 1.0)) <= TRACE_TOL and np.max(np.abs(tw - 1.0)) <= TRACE_TOL
 
 
+def test_adaptive_run_with_rejection_multi_tile_vs_compiled_reference(ref):
+    """An adaptive run with a rejected step, at a size where every block walks
+    several tiles (1024 x 256 beams: refilled tile rings, a partial last tile,
+    the inter-stage stashes rewritten after each rejection): the same
+    accept/reject sequence and the same state as the unmodified reference
+    engine (lane_body, solver.cpp:414-456)."""
+    cfg = baseline_config("configs2", Abins=1024, R0=50, Rn=60, dr=2e-3, max_dr=1e-2, Ts=24)
+    cfg.override("eps0=1e-11")
+    env, eng = make(cfg)
+    assert eng.launch_mode == Engine.LAUNCH_STAGES
+    s = eng.run(StepControl.from_config(cfg))
+    want, summ = ref.run(cfg.render(), lanes=min(os.cpu_count() or 1, 16))
+    assert s.rejected >= 1 and s.accepted >= 20, s
+    assert (s.iterations, s.accepted, s.rejected) == (summ["iterations"], summ["accepted"], summ["rejected"])
+    assert s.final_r == pytest.approx(summ["final_r"], rel=1e-12)
+    (rg, tg), (rw, tw) = density(eng.state(), env.ebins), density(want, env.ebins)
+    assert np.max(np.abs(rg - rw)) <= RHO_TOL
+    assert np.max(np.abs(tg - tw)) <= 10 * TRACE_TOL
+
+
 @pytest.mark.parametrize("name,kw", [
     ("configs3", dict(R0=0.0, Rn=1.0, dr=1e-7, max_dr=1e-7, Ts=3)),  # (dr = 1e-6: trace drifts 1.6e-12 in the oracle too)
     ("configs4", dict(R0=30.0, Rn=31.0, dr=1e-6, max_dr=1e-6, Ts=3)),
